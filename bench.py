@@ -1,0 +1,362 @@
+"""Benchmark: range-image segmentation throughput on B200 (BASELINE.json metric).
+
+Workload (default): BASELINE config 1 — 256 independent 64x2048 float32 frames
+(seeds 0-255 per rank), reference default parameters (ground removal on,
+d_max 0.8 m, theta 10 deg, min_cluster_points 100, skip count S = 0, i.e. no
+Map Connections).  One step = one fused kernel launch over the whole batch.
+
+Prints ONE JSON line (rank 0).  ``value`` = frames/s over all ranks with the
+inputs resident in HBM; ``e2e`` = the same metric through the host-buffer C
+ABI (``rs_segment_batch_host``: pinned host ranges in, labels / counts / sizes
+back to the host, copies inside the timed region); ``roofline`` = the kernel's
+algorithmic bytes (16.5 B/cell) / its event-timed duration
+against the measured HBM copy bandwidth; ``cpu_baseline`` = the CPU oracle
+port of the reference path on this host's cores.
+
+``--impl reference`` times the CPU oracle (the reference algorithm restated
+in C, oracle/) with all host threads on the same workload and metric.
+
+Multi-GPU (torchrun): each rank segments its own 256 frames (weak scaling,
+no collective on the data path — frames are independent); the step time is
+the max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+ALGO_BYTES_PER_CELL = 16.5          # 4 in + 4 out + 0.5 edge bits + 8 label scratch
+MC_BYTES_PER_OFFSET = 0.25
+COMPULSORY_BYTES_PER_CELL = 8.0
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    p.add_argument("--config", type=int, default=1, help="BASELINE config id (0-4)")
+    p.add_argument("--skip", type=int, default=0, help="skip count S (0 = reference default)")
+    p.add_argument("--core", action="store_true", help="ground off, min_cluster_points 1")
+    p.add_argument("--rows-per-cta", type=int, default=0)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--cpu-seconds", type=float, default=10.0)
+    return p.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)),
+            int(os.environ.get("WORLD_SIZE", 1)))
+
+
+def pipeline_config(args):
+    import paper_2003_00575_b200 as rs
+    if args.core:
+        return rs.PipelineConfig(mc_pattern=rs.skip_pattern(args.skip), ground_removal=False,
+                                 min_cluster_points=1)
+    return rs.PipelineConfig(mc_pattern=rs.skip_pattern(args.skip))
+
+
+def workload_config(args, spec, batch, world):
+    return {
+        "workload": f"BASELINE config {args.config}: {spec.name}",
+        "frames_per_gpu": batch, "H": spec.H, "W": spec.W,
+        "cells_per_gpu": batch * spec.H * spec.W,
+        "params": ("core: ground off, min_cluster_points 1" if args.core else
+                   "reference defaults: ground on, d_max 0.8, theta 10, min_cluster_points 100")
+                  + f", skip S={args.skip}",
+        "l2": "flushed between timed steps (512 MiB write); inputs 134 MB > L2 as well",
+        "parallelism": f"replicas x{world} (independent frames, no collective)",
+    }
+
+
+def measured_peak():
+    f = ROOT / "MEASURED_PEAKS.json"
+    if f.exists():
+        try:
+            return float(json.loads(f.read_text())["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+        except Exception:
+            pass
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_sample(frames_np, packed, seconds, nthreads=1):
+    """Time the oracle port on whole frames until ~`seconds` of CPU work."""
+    from oracle import oracle
+    B = frames_np.shape[0]
+    done, t0 = 0, time.perf_counter()
+    chunk = max(1, nthreads)
+    i = 0
+    while True:
+        sl = frames_np[i:i + chunk]
+        oracle.segment_batch(sl, packed, nthreads=nthreads)
+        done += sl.shape[0]
+        i = (i + chunk) % B
+        el = time.perf_counter() - t0
+        if el >= seconds:
+            return done, el
+
+
+def run_reference(args):
+    """CPU arm: the reference algorithm (C oracle port) on all host threads."""
+    rank, _, world = dist_env()
+    if rank != 0:
+        return
+    import numpy as np  # noqa: F401
+    import torch
+    import paper_2003_00575_b200 as rs
+    from oracle import oracle
+    from paper_2003_00575_b200 import synthetic
+    spec = synthetic.CONFIGS[args.config]
+    frames = synthetic.make_batch(args.config, device="cuda" if torch.cuda.is_available() else "cpu")
+    frames_np = frames.cpu().numpy()
+    packed = rs.pack_tables(synthetic.sensor_for(spec), pipeline_config(args))
+    nthreads = os.cpu_count() or 1
+    B = frames_np.shape[0]
+    # each step = a bounded sample of the workload: as many whole frames as
+    # the host does in ~0.5 s (at least one per thread)
+    t0 = time.perf_counter()
+    oracle.segment_batch(frames_np[:nthreads], packed, nthreads=nthreads)
+    per_frame = (time.perf_counter() - t0) / min(nthreads, B) * nthreads
+    sample = max(nthreads, min(B, int(0.5 / max(per_frame, 1e-6) * nthreads)))
+    for _ in range(args.warmup):
+        oracle.segment_batch(frames_np[:sample], packed, nthreads=nthreads)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        oracle.segment_batch(frames_np[:sample], packed, nthreads=nthreads)
+        times.append(time.perf_counter() - t0)
+    tot = sum(times)
+    fps = args.steps * sample / tot
+    cells = spec.H * spec.W
+    line = {
+        "impl": "reference", "metric": "frames/s", "value": fps, "unit": "frames/s",
+        "points_per_s": fps * cells, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": tot / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded BASELINE generator)",
+        "config": workload_config(args, spec, B, 1),
+        "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": nthreads, "kind": "port",
+                         "sample": f"{sample} of the {B} frames per step, oracle/rangeseg_oracle.c "
+                                   f"(reference algorithm restated in C), {nthreads} threads"},
+        "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_b200(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    import paper_2003_00575_b200 as rs
+    from paper_2003_00575_b200 import synthetic
+
+    rank, local_rank, world = dist_env()
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    spec = synthetic.CONFIGS[args.config]
+    B = spec.batch
+    frames = synthetic.make_batch(args.config, device=dev, first_seed=rank * B)
+    model = synthetic.sensor_for(spec)
+    cfg = pipeline_config(args)
+    pipe = rs.Pipeline(model, cfg, device=dev, rows_per_cta=args.rows_per_cta)
+    labels = torch.empty((B, spec.H, spec.W), dtype=torch.int32, device=dev)
+    ncl = torch.empty((B,), dtype=torch.int32, device=dev)
+    sizes = torch.empty((B, pipe.sizes_stride), dtype=torch.int64, device=dev)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        pipe.segment_batch(frames, labels=labels, n_clusters=ncl, cluster_sizes=sizes)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local_rank) as clk:
+        wall0 = time.perf_counter()
+        for i in range(args.steps):
+            flush.zero_()                        # evict L2 between steps
+            starts[i].record(stream)
+            step()
+            ends[i].record(stream)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - wall0
+    if world > 1:
+        dist.barrier()
+    kern_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    ms = sum(kern_ms) / len(kern_ms)
+    t = torch.tensor([ms], device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+
+    cells = B * spec.H * spec.W
+    fps = world * B / (ms_max * 1e-3)
+    algo_bytes = cells * (ALGO_BYTES_PER_CELL + MC_BYTES_PER_OFFSET * len(cfg.mc_pattern))
+    peak, peak_src = measured_peak()
+    achieved = algo_bytes / (ms * 1e-3) / 1e9
+
+    # ---- end to end through the host-buffer C ABI --------------------------
+    e2e = None
+    if not args.no_e2e:
+        host_in = torch.empty((B, spec.H, spec.W), dtype=torch.float32, pin_memory=True)
+        host_in.copy_(frames)
+        h_in = host_in.numpy()
+        h_lab = torch.empty((B, spec.H, spec.W), dtype=torch.int32, pin_memory=True).numpy()
+        h_ncl = torch.empty((B,), dtype=torch.int32, pin_memory=True).numpy()
+        h_sz = torch.empty((B, pipe.sizes_stride), dtype=torch.int64, pin_memory=True).numpy()
+        for _ in range(max(args.warmup, 3)):
+            pipe.segment_batch_host(h_in, h_lab, h_ncl, h_sz)
+        if world > 1:
+            dist.barrier()
+        e_times = []
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            pipe.segment_batch_host(h_in, h_lab, h_ncl, h_sz)
+            e_times.append(time.perf_counter() - t0)
+        te = torch.tensor([sum(e_times) / len(e_times)], device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": world * B / float(te.item()), "unit": "frames/s",
+               "h2d_bytes_per_step": int(h_in.nbytes + pipe._tables_host.nbytes),
+               "d2h_bytes_per_step": int(h_lab.nbytes + h_ncl.nbytes + h_sz.nbytes),
+               "path": "rs_segment_batch_host (C ABI), pinned host buffers, 2 streams"}
+        # e2e results must equal the device path
+        assert np.array_equal(h_lab, labels.cpu().numpy()), "e2e labels differ from device path"
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    cpu = None
+    if not args.no_cpu_baseline:
+        done, el = cpu_sample(frames.cpu().numpy(), pipe.packed, args.cpu_seconds, 1)
+        cpu = {"value": done / el, "unit": "frames/s", "cores": 1, "kind": "port",
+               "sample": f"{done} frames of this workload, single thread, oracle/rangeseg_oracle.c "
+                         f"(reference algorithm restated in C), {el:.1f} s"}
+
+    traffic = None
+    tf = ROOT / "profiles" / "kernel_traffic.json"
+    if tf.exists():
+        try:
+            traffic = json.loads(tf.read_text()).get(f"config{args.config}" + ("_core" if args.core else "")
+                                                     + (f"_S{args.skip}" if args.skip else ""))
+        except Exception:
+            traffic = None
+
+    line = {
+        "metric": "frames/s", "value": fps, "unit": "frames/s",
+        "points_per_s": fps * spec.H * spec.W,
+        "valid_points_per_s": fps * float((frames > 0).float().mean()) * spec.H * spec.W,
+        "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3),
+        "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded BASELINE generator)",
+        "config": workload_config(args, spec, B, world),
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "algorithmic_bytes_per_launch": algo_bytes,
+                     "bytes_per_cell": algo_bytes / cells,
+                     "compulsory_frac": cells * COMPULSORY_BYTES_PER_CELL / (ms * 1e-3) / 1e9 / peak,
+                     "peak_source": peak_src, "kernel": "rs_segment_kernel",
+                     "kernel_ms": ms},
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": args.steps,
+        "clocks": clk.summary(),
+        "wall_s_timed_region": wall,
+        "plan": {"rows_per_cta": pipe.rows_per_cta, "ctas_per_frame": pipe.ctas_per_frame,
+                 "smem_bytes": pipe.smem_bytes},
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

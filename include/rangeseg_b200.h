@@ -1,0 +1,105 @@
+/*
+ * rangeseg_b200.h — C ABI of the B200 range-image segmentation path.
+ *
+ * Drop-in boundary for the reference's clustering entry point
+ * (/root/reference/pkg/src/rangeseg/pipeline.py):
+ *
+ *   rs_segment_batch       replaces Pipeline.segment_range_image (pipeline.py:85-131)
+ *                          for B frames at once; its multi-frame analogue in the
+ *                          reference is segment_in_parallel (pipeline.py:170-197).
+ *                          Device pointers, stream-ordered.
+ *   rs_segment_batch_host  the same call on HOST buffers (copies in/out inside),
+ *                          the shape a cgo/ctypes/JNI binding would use.
+ *   rs_stage_masks         replaces extract_ground (ground.py:95-141) +
+ *                          build_connectivity (connectivity.py:64-92): the
+ *                          per-pixel ground mask and edge images, for parity
+ *                          checks of the edge decisions on their own.
+ *
+ * All entry points return RS_OK (0) or a status code; rs_last_error() gives a
+ * message for the calling thread.  Invalid arguments are rejected before any
+ * launch, mirroring the reference's ValueError conditions (ccl.py:71-72,
+ * ground.py:108-110, map_connections.py:152-153, sensor.py:151-155).
+ *
+ * Constant tables (float32, `tables` argument): computed in float64 and cast
+ * once, exactly as the reference does, laid out as
+ *   sin_ch[H] | sin_a[H-1] | cos_a[H-1] | lo[H-1] | hi[H-1] | two_cos_v[H-1]
+ *   | two_cos_off[k][H] for k < n_offsets (indexed by the pair's upper row)
+ * rs_tables_count(H, n_offsets) gives its length in floats.
+ *
+ * Output contract (bit-exact with the reference):
+ *   labels[b][r][c]   int32, 0 = background (invalid, ground or filtered);
+ *                     clusters numbered 1..K in first-encounter row-major order
+ *   n_clusters[b]     K
+ *   cluster_sizes[b][0..K]  int64 (optional, may be NULL); [0] = H*W - sum of
+ *                     kept sizes; sizes_stride must be >= H*W/max(min,1) + 1
+ */
+#ifndef RANGESEG_B200_H
+#define RANGESEG_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RS_MAX_OFFSETS 32
+
+enum rs_status {
+    RS_OK = 0,
+    RS_EINVAL = 1,      /* bad shape / parameter / offset (reference: ValueError) */
+    RS_ECUDA = 2,       /* CUDA runtime error (reference: n/a) */
+    RS_ETOOLARGE = 3,   /* frame does not fit one thread-block cluster */
+    RS_ENODEV = 4       /* no CUDA device */
+};
+
+typedef struct rs_config {
+    int32_t height, width;                  /* H, W of every frame */
+    int32_t n_offsets;                      /* Map Connection offsets (MCPattern) */
+    int32_t offsets[RS_MAX_OFFSETS][2];     /* canonical (dy, dx): dy>0, or dy==0 && dx>0 */
+    int32_t min_cluster_points;             /* filter_small threshold (<=1: no filter) */
+    int32_t ground_removal;                 /* PipelineConfig.ground_removal */
+    float d_max_sq;                         /* f32(d_max*d_max) */
+    float mount_height;                     /* f32(model.mount_height) */
+    float keep_above;                       /* f32(GroundParams.resolve_keep_above) */
+    float two_cos_h;                        /* f32(pair_constant(0, 1)) */
+    int32_t rows_per_cta;                   /* 0 = automatic band height */
+    int32_t reserved[3];
+} rs_config;
+
+/* Number of floats in the constant-table block. */
+size_t rs_tables_count(int32_t height, int32_t n_offsets);
+
+/* Launch geometry the library would use for cfg (rows per CTA band, CTAs per
+ * frame = cluster size, dynamic shared memory per CTA). */
+int rs_plan(const rs_config *cfg, int32_t *rows_per_cta, int32_t *ctas_per_frame,
+            size_t *smem_bytes);
+
+/* B frames, device pointers, enqueued on `stream` (a cudaStream_t; NULL = legacy
+ * default stream).  Asynchronous: returns after the launch. */
+int rs_segment_batch(const rs_config *cfg, const float *d_tables, const float *d_ranges,
+                     int32_t batch, int32_t *d_labels, int32_t *d_n_clusters,
+                     int64_t *d_cluster_sizes, int64_t sizes_stride, void *stream);
+
+/* Same on host buffers (pinned memory gives overlapped copies).  Synchronous. */
+int rs_segment_batch_host(const rs_config *cfg, const float *h_tables, const float *h_ranges,
+                          int32_t batch, int32_t *h_labels, int32_t *h_n_clusters,
+                          int64_t *h_cluster_sizes, int64_t sizes_stride);
+
+/* Stage outputs for parity checks: ground mask [B][H][W] (1 = ground or no
+ * return), horizontal [B][H][W], vertical [B][H-1][W]; uint8, device. */
+int rs_stage_masks(const rs_config *cfg, const float *d_tables, const float *d_ranges,
+                   int32_t batch, uint8_t *d_ground, uint8_t *d_horizontal,
+                   uint8_t *d_vertical, void *stream);
+
+/* Message for the last non-OK status returned on this thread. */
+const char *rs_last_error(void);
+
+/* ABI version (major*100 + minor). */
+int rs_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RANGESEG_B200_H */

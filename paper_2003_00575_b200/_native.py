@@ -1,0 +1,100 @@
+"""ctypes binding of the C ABI in include/rangeseg_b200.h.
+
+The shared library is built in-tree by :mod:`.build` (``__graft_entry__.build()``).
+There is no CPU fallback: if the library is missing, or no CUDA device is
+present when a kernel is requested, calls raise ``RuntimeError``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from pathlib import Path
+
+LIB_PATH = Path(__file__).resolve().parent / "_lib" / "librangeseg_b200.so"
+MAX_OFFSETS = 32
+
+RS_OK, RS_EINVAL, RS_ECUDA, RS_ETOOLARGE, RS_ENODEV = range(5)
+
+EXPORTS = ("rs_tables_count", "rs_plan", "rs_segment_batch", "rs_segment_batch_host",
+           "rs_stage_masks", "rs_last_error", "rs_version")
+
+
+class RsConfig(ctypes.Structure):
+    _fields_ = [("height", ctypes.c_int32), ("width", ctypes.c_int32),
+                ("n_offsets", ctypes.c_int32),
+                ("offsets", (ctypes.c_int32 * 2) * MAX_OFFSETS),
+                ("min_cluster_points", ctypes.c_int32),
+                ("ground_removal", ctypes.c_int32),
+                ("d_max_sq", ctypes.c_float), ("mount_height", ctypes.c_float),
+                ("keep_above", ctypes.c_float), ("two_cos_h", ctypes.c_float),
+                ("rows_per_cta", ctypes.c_int32),
+                ("reserved", ctypes.c_int32 * 3)]
+
+
+_lib = None
+
+_P = ctypes.c_void_p
+
+
+def lib():
+    """Load the native library (raises if it was not built)."""
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise RuntimeError(
+                f"native library {LIB_PATH} is missing; run __graft_entry__.build() "
+                "(there is no CPU fallback)")
+        L = ctypes.CDLL(str(LIB_PATH))
+        L.rs_tables_count.restype = ctypes.c_size_t
+        L.rs_tables_count.argtypes = [ctypes.c_int32, ctypes.c_int32]
+        L.rs_plan.restype = ctypes.c_int
+        L.rs_plan.argtypes = [ctypes.POINTER(RsConfig), ctypes.POINTER(ctypes.c_int32),
+                              ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_size_t)]
+        L.rs_segment_batch.restype = ctypes.c_int
+        L.rs_segment_batch.argtypes = [ctypes.POINTER(RsConfig), _P, _P, ctypes.c_int32,
+                                       _P, _P, _P, ctypes.c_int64, _P]
+        L.rs_segment_batch_host.restype = ctypes.c_int
+        L.rs_segment_batch_host.argtypes = [ctypes.POINTER(RsConfig), _P, _P, ctypes.c_int32,
+                                            _P, _P, _P, ctypes.c_int64]
+        L.rs_stage_masks.restype = ctypes.c_int
+        L.rs_stage_masks.argtypes = [ctypes.POINTER(RsConfig), _P, _P, ctypes.c_int32,
+                                     _P, _P, _P, _P]
+        L.rs_last_error.restype = ctypes.c_char_p
+        L.rs_version.restype = ctypes.c_int
+        _lib = L
+    return _lib
+
+
+def check(status: int, what: str = "rangeseg_b200"):
+    """Map a C status to the reference's exception types."""
+    if status == RS_OK:
+        return
+    msg = lib().rs_last_error().decode(errors="replace")
+    if status in (RS_EINVAL, RS_ETOOLARGE):
+        raise ValueError(f"{what}: {msg}")
+    raise RuntimeError(f"{what}: {msg}")
+
+
+def make_config(packed, rows_per_cta: int = 0) -> RsConfig:
+    if len(packed.offsets) > MAX_OFFSETS:
+        raise ValueError(f"at most {MAX_OFFSETS} Map Connection offsets are supported")
+    cfg = RsConfig()
+    cfg.height, cfg.width = packed.height, packed.width
+    cfg.n_offsets = len(packed.offsets)
+    for i, (dy, dx) in enumerate(packed.offsets):
+        cfg.offsets[i][0], cfg.offsets[i][1] = dy, dx
+    cfg.min_cluster_points = int(packed.min_cluster_points)
+    cfg.ground_removal = int(bool(packed.ground_removal))
+    cfg.d_max_sq = float(packed.d_max_sq)
+    cfg.mount_height = float(packed.mount)
+    cfg.keep_above = float(packed.keep_above)
+    cfg.two_cos_h = float(packed.two_cos_h)
+    cfg.rows_per_cta = int(rows_per_cta)
+    return cfg
+
+
+def plan(cfg: RsConfig):
+    R, C, smem = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_size_t()
+    check(lib().rs_plan(ctypes.byref(cfg), ctypes.byref(R), ctypes.byref(C), ctypes.byref(smem)),
+          "rs_plan")
+    return R.value, C.value, smem.value

@@ -1,0 +1,30 @@
+"""Run the fused kernel a few times on one config (for ncu / compute-sanitizer)."""
+import argparse
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+
+import torch
+
+import paper_2003_00575_b200 as rs
+from paper_2003_00575_b200 import synthetic
+
+p = argparse.ArgumentParser()
+p.add_argument("--config", type=int, default=1)
+p.add_argument("--batch", type=int, default=64)
+p.add_argument("--iters", type=int, default=3)
+p.add_argument("--skip", type=int, default=0)
+p.add_argument("--core", action="store_true")
+p.add_argument("--rows", type=int, default=0)
+a = p.parse_args()
+spec = synthetic.CONFIGS[a.config]
+frames = synthetic.make_batch(a.config, a.batch, device="cuda")
+cfg = (rs.PipelineConfig(mc_pattern=rs.skip_pattern(a.skip), ground_removal=False, min_cluster_points=1)
+       if a.core else rs.PipelineConfig(mc_pattern=rs.skip_pattern(a.skip)))
+pipe = rs.Pipeline(synthetic.sensor_for(spec), cfg, rows_per_cta=a.rows)
+torch.cuda.synchronize()
+for _ in range(a.iters):
+    pipe.segment_batch(frames)
+torch.cuda.synchronize()
+print("ok", pipe.rows_per_cta, pipe.ctas_per_frame, pipe.smem_bytes)

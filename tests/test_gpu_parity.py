@@ -1,0 +1,254 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the reference's
+recorded outputs (tests/golden) and against the CPU oracle on the five
+BASELINE configs.  Bar: bit-exact int32 labels and int64 cluster sizes
+(integer work), bit-exact ground / edge masks (float32 decisions computed in
+the reference's op order — the 1e-6 tolerance band of north_star is not used,
+the count of mismatches must be 0)."""
+
+import numpy as np
+import pytest
+import torch
+
+import golden
+import paper_2003_00575_b200 as rs
+from oracle import oracle
+from paper_2003_00575_b200 import synthetic
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(model, cfg, frames, **kw):
+    pipe = rs.Pipeline(model, cfg, device="cuda:0", **kw)
+    x = torch.as_tensor(np.ascontiguousarray(frames, dtype=np.float32)).cuda()
+    if x.dim() == 2:
+        x = x[None]
+    res = pipe.segment_batch(x)
+    torch.cuda.synchronize()
+    return pipe, res
+
+
+def _assert_frame(res, b, labels, sizes):
+    got = res.label_image(b)
+    assert np.array_equal(got.labels, labels), \
+        f"{int((got.labels != labels).sum())} label mismatches"
+    assert np.array_equal(got.cluster_sizes, sizes)
+
+
+# ---------------------------------------------------------------- golden -----
+@pytest.mark.parametrize("case_key,frame_key", golden.frame_cases())
+def test_golden_frames(case_key, frame_key, cuda):
+    m, cfg, ranges, labels, sizes, stages = golden.case("frames", case_key, frame_key)
+    pipe, res = _run(m, cfg, ranges)
+    _assert_frame(res, 0, labels, sizes)
+    if stages is not None:
+        g, h, v = pipe.stage_masks(torch.from_numpy(ranges).cuda()[None])
+        for got, want in zip((g, h, v), stages):
+            assert int((got[0].cpu().numpy() != want).sum()) == 0
+
+
+@pytest.mark.parametrize("key", golden.random_cases())
+@pytest.mark.parametrize("rows", [0, 1, 2])
+def test_golden_random_frames(key, rows, cuda):
+    m, cfg, ranges, labels, sizes, stages = golden.case("random", key)
+    if rows and -(-m.height // rows) > 16:
+        pytest.skip("more bands than a cluster holds")
+    pipe, res = _run(m, cfg, ranges, rows_per_cta=rows)
+    _assert_frame(res, 0, labels, sizes)
+    g, h, v = pipe.stage_masks(torch.from_numpy(ranges).cuda()[None])
+    for got, want in zip((g, h, v), stages):
+        assert np.array_equal(got[0].cpu().numpy(), want)
+
+
+# --------------------------------------------------- BASELINE configs vs oracle
+VARIANTS = {
+    "default": rs.PipelineConfig(),
+    "core": rs.PipelineConfig(ground_removal=False, min_cluster_points=1),
+    "S1": rs.PipelineConfig(mc_pattern=rs.skip_pattern(1)),
+    "mc14_core": rs.PipelineConfig(mc_pattern=rs.preset_pattern("mc14"),
+                                   ground_removal=False, min_cluster_points=1),
+}
+
+
+@pytest.fixture(scope="module")
+def config_frames():
+    out = {}
+    for cid, n in ((0, 1), (1, 12), (2, 6), (3, 24), (4, 12)):
+        out[cid] = synthetic.make_batch(cid, n, device="cuda:0")
+    return out
+
+
+@pytest.mark.parametrize("variant", list(VARIANTS))
+@pytest.mark.parametrize("cid", [0, 1, 2, 3, 4])
+def test_configs_vs_oracle(cid, variant, config_frames):
+    model = synthetic.sensor_for(synthetic.CONFIGS[cid])
+    cfg = VARIANTS[variant]
+    frames = config_frames[cid]
+    pipe = rs.Pipeline(model, cfg, device="cuda:0")
+    res = pipe.segment_batch(frames)
+    host = frames.cpu().numpy()
+    want_l, want_n, want_s = oracle.segment_batch(host, pipe.packed, sizes_stride=pipe.sizes_stride)
+    torch.cuda.synchronize()
+    got_l = res.labels.cpu().numpy()
+    got_n = res.n_clusters.cpu().numpy()
+    got_s = res.cluster_sizes.cpu().numpy()
+    assert np.array_equal(got_n, want_n)
+    assert int((got_l != want_l).sum()) == 0
+    for b in range(host.shape[0]):
+        k = int(want_n[b])
+        assert np.array_equal(got_s[b, :k + 1], want_s[b, :k + 1])
+
+
+@pytest.mark.parametrize("rows", [1, 3, 5, 8, 16])
+def test_band_height_does_not_change_labels(rows, config_frames):
+    model = synthetic.sensor_for(synthetic.CONFIGS[1])
+    frames = config_frames[1][:4]
+    cfg = rs.PipelineConfig(mc_pattern=rs.preset_pattern("mc6"), ground_removal=False,
+                            min_cluster_points=3)
+    if -(-64 // rows) > 16:
+        pytest.skip("more bands than a cluster holds")
+    base = rs.Pipeline(model, cfg, device="cuda:0").segment_batch(frames)
+    alt = rs.Pipeline(model, cfg, device="cuda:0", rows_per_cta=rows).segment_batch(frames)
+    torch.cuda.synchronize()
+    assert torch.equal(base.labels, alt.labels)
+    assert torch.equal(base.n_clusters, alt.n_clusters)
+
+
+def test_full_headline_batch_vs_oracle(cuda):
+    """Config 1 at its full size (256 frames, 2^25 cells), reference defaults."""
+    frames = synthetic.make_batch(1, device="cuda:0")
+    model = synthetic.sensor_for(synthetic.CONFIGS[1])
+    pipe = rs.Pipeline(model, rs.PipelineConfig(), device="cuda:0")
+    res = pipe.segment_batch(frames)
+    want_l, want_n, want_s = oracle.segment_batch(frames.cpu().numpy(), pipe.packed,
+                                                  sizes_stride=pipe.sizes_stride)
+    torch.cuda.synchronize()
+    assert np.array_equal(res.n_clusters.cpu().numpy(), want_n)
+    assert int((res.labels.cpu().numpy() != want_l).sum()) == 0
+    got_s = res.cluster_sizes.cpu().numpy()
+    for b in range(frames.shape[0]):
+        k = int(want_n[b])
+        assert np.array_equal(got_s[b, :k + 1], want_s[b, :k + 1])
+
+
+# ------------------------------------------------------------------ edges ---
+def _random_model(H, W):
+    return rs.SensorModel(-2.0 - 1.0 * np.arange(H), 360.0 / W, 1.7, width=W)
+
+
+@pytest.mark.parametrize("H,W", [(2, 1), (2, 2), (3, 1), (2, 33), (17, 3), (64, 5), (5, 2048),
+                                 (31, 31), (40, 700)])
+def test_odd_shapes_vs_oracle(H, W, rng, cuda):
+    model = _random_model(H, W)
+    frames = rng.uniform(0.5, 12.0, size=(3, H, W)).astype(np.float32)
+    frames[rng.random(frames.shape) < 0.3] = 0
+    for cfg in (rs.PipelineConfig(ground_removal=False, min_cluster_points=1),
+                rs.PipelineConfig(ground_removal=False, min_cluster_points=2,
+                                  mc_pattern=rs.MCPattern(tuple(
+                                      o for o in ((0, 2), (1, -1), (1, 1), (2, 0))
+                                      if o[0] < H and abs(o[1]) < W)))):
+        pipe, res = _run(model, cfg, frames)
+        for b in range(3):
+            wl, ws = oracle.segment_frame(frames[b], pipe.packed)
+            _assert_frame(res, b, wl, ws)
+
+
+def test_empty_and_full_frames(cuda):
+    model = synthetic.sensor_for(synthetic.CONFIGS[0])
+    frames = np.zeros((3, 64, 2048), np.float32)
+    frames[1] = 10.0                              # one wrap-around component
+    frames[2, :, ::2] = 10.0                      # isolated vertical lines
+    for cfg in (rs.PipelineConfig(ground_removal=False, min_cluster_points=1),
+                rs.PipelineConfig(ground_removal=False, min_cluster_points=65)):
+        pipe, res = _run(model, cfg, frames)
+        for b in range(3):
+            wl, ws = oracle.segment_frame(frames[b], pipe.packed)
+            _assert_frame(res, b, wl, ws)
+    assert int(res.n_clusters[0]) == 0
+    assert int(res.n_clusters[1]) == 1
+
+
+def test_serpentine_component(cuda):
+    """A single snake through every row: the longest possible cross-band chain."""
+    H, W = 64, 256
+    model = _random_model(H, W)
+    f = np.zeros((H, W), np.float32)
+    for r in range(0, H, 2):
+        f[r, :] = 5.0
+        f[r + 1, (W - 1) if (r // 2) % 2 == 0 else 0] = 5.0 if r + 1 < H else 0
+    f[:, 1::17] = 0.0
+    cfg = rs.PipelineConfig(ground_removal=False, min_cluster_points=1)
+    for rows in (1, 4, 8):
+        pipe, res = _run(model, cfg, f, rows_per_cta=rows)
+        wl, ws = oracle.segment_frame(f, pipe.packed)
+        _assert_frame(res, 0, wl, ws)
+
+
+def test_rotation_equivariance(config_frames):
+    model = synthetic.sensor_for(synthetic.CONFIGS[1])
+    f = config_frames[1][:2]
+    cfg = rs.PipelineConfig(ground_removal=False, min_cluster_points=1)
+    pipe = rs.Pipeline(model, cfg, device="cuda:0")
+    a = pipe.segment_batch(f).labels.cpu().numpy()
+    b = pipe.segment_batch(torch.roll(f, 731, dims=2)).labels.cpu().numpy()
+    for i in range(2):
+        ra = np.roll(a[i], 731, axis=1)
+        # same partition up to naming
+        pairs = set(zip(ra.ravel().tolist(), b[i].ravel().tolist()))
+        assert len(pairs) == len(set(ra.ravel().tolist()))
+
+
+def test_determinism(config_frames):
+    model = synthetic.sensor_for(synthetic.CONFIGS[4])
+    pipe = rs.Pipeline(model, rs.PipelineConfig(ground_removal=False, min_cluster_points=1,
+                                                mc_pattern=rs.preset_pattern("mc1")),
+                       device="cuda:0")
+    outs = [pipe.segment_batch(config_frames[4]).labels.clone() for _ in range(3)]
+    assert all(torch.equal(outs[0], o) for o in outs[1:])
+
+
+# --------------------------------------------------------------- host API ---
+def test_segment_range_image_api(cuda):
+    m, cfg, ranges, labels, sizes, _ = golden.case("frames", "occluder/mc1", "occluder")
+    li, rec = rs.Pipeline(m, cfg).segment_range_image(rs.from_ranges(ranges))
+    assert np.array_equal(li.labels, labels)
+    assert np.array_equal(li.cluster_sizes, sizes)
+    assert li.cluster_count == 2
+    assert rec.stage_sum() <= rec.total + 0.5
+    with pytest.raises(ValueError):
+        rs.Pipeline(m, cfg).segment_range_image(rs.from_ranges(ranges[:, :10]))
+
+
+def test_segment_in_parallel_matches_serial(cuda):
+    m, cfg, a, *_ = golden.case("frames", "twobox/default", "twobox")
+    _, _, b, *_ = golden.case("frames", "occluder/default", "occluder")
+    frames = [a, b, a]
+    serial = [rs.Pipeline(m, cfg).segment_range_image(rs.from_ranges(f))[0] for f in frames]
+    par = rs.segment_in_parallel(frames, m, cfg)
+    for s, p in zip(serial, par):
+        assert np.array_equal(s.labels, p.labels)
+        assert np.array_equal(s.cluster_sizes, p.cluster_sizes)
+
+
+def test_host_buffer_entry_matches_device(config_frames):
+    model = synthetic.sensor_for(synthetic.CONFIGS[1])
+    pipe = rs.Pipeline(model, rs.PipelineConfig(), device="cuda:0")
+    f = config_frames[1]
+    dev = pipe.segment_batch(f)
+    host = torch.empty(f.shape, dtype=torch.float32, pin_memory=True)
+    host.copy_(f)
+    lab, ncl, sz = pipe.segment_batch_host(host.numpy())
+    torch.cuda.synchronize()
+    assert np.array_equal(lab, dev.labels.cpu().numpy())
+    assert np.array_equal(ncl, dev.n_clusters.cpu().numpy())
+    assert np.array_equal(sz, dev.cluster_sizes.cpu().numpy())
+
+
+def test_batch_zero_and_errors(cuda):
+    model = synthetic.sensor_for(synthetic.CONFIGS[3])
+    pipe = rs.Pipeline(model, device="cuda:0")
+    res = pipe.segment_batch(torch.zeros((0, 32, 1024), device="cuda:0"))
+    assert res.labels.shape == (0, 32, 1024)
+    with pytest.raises(ValueError):
+        pipe.segment_batch(torch.zeros((1, 32, 1000), device="cuda:0"))
+    with pytest.raises(ValueError):
+        pipe.segment_batch(torch.zeros((1, 32, 1024), device="cuda:0", dtype=torch.float64))

@@ -1,0 +1,47 @@
+"""The CPU oracle (oracle/rangeseg_oracle.c) against the reference's own outputs.
+
+tests/golden/*.npz hold what the Python reference (rangeseg, run in the build
+container by tests/golden/make_golden.py) returned for these inputs; here the
+oracle must reproduce labels, cluster sizes and the ground/edge stage masks
+bit for bit.  This pins the oracle before any GPU test trusts it.
+"""
+
+import numpy as np
+import pytest
+
+import golden
+from oracle import oracle
+from paper_2003_00575_b200 import pack_tables
+
+
+@pytest.mark.parametrize("case_key,frame_key", golden.frame_cases())
+def test_oracle_matches_reference_on_frames(case_key, frame_key):
+    m, cfg, ranges, labels, sizes, stages = golden.case("frames", case_key, frame_key)
+    got = oracle.segment_frame(ranges, pack_tables(m, cfg), stages=True)
+    assert np.array_equal(got[0], labels)
+    assert np.array_equal(got[1], sizes)
+    if stages is not None:
+        for g, w in zip(got[2:], stages):
+            assert np.array_equal(g, w)
+
+
+@pytest.mark.parametrize("key", golden.random_cases())
+def test_oracle_matches_reference_on_random_frames(key):
+    m, cfg, ranges, labels, sizes, stages = golden.case("random", key)
+    got = oracle.segment_frame(ranges, pack_tables(m, cfg), stages=True)
+    assert np.array_equal(got[0], labels)
+    assert np.array_equal(got[1], sizes)
+    for g, w in zip(got[2:], stages):
+        assert np.array_equal(g, w)
+
+
+def test_oracle_batch_equals_per_frame():
+    m, cfg, ranges, *_ = golden.case("frames", "c0/mc1", "c0")
+    pt = pack_tables(m, cfg)
+    frames = np.stack([ranges, np.roll(ranges, 100, axis=1), ranges[::-1].copy() * 0])
+    lab, ncl, sz = oracle.segment_batch(frames, pt, nthreads=2)
+    for b in range(3):
+        l1, s1 = oracle.segment_frame(frames[b], pt)
+        assert np.array_equal(lab[b], l1)
+        assert ncl[b] == len(s1) - 1
+        assert np.array_equal(sz[b, :len(s1)], s1)
