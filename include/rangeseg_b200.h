@@ -92,6 +92,11 @@ int rs_stage_masks(const rs_config *cfg, const float *d_tables, const float *d_r
                    int32_t batch, uint8_t *d_ground, uint8_t *d_horizontal,
                    uint8_t *d_vertical, void *stream);
 
+/* Debug: per-CTA phase timestamps (clock64, 16 slots per CTA) of the last
+ * launch.  Only a library built with -DRS_PHASE_PROF records them; the
+ * production build returns RS_EINVAL. */
+int rs_phase_profile(int64_t *host_out, int32_t max_ctas);
+
 /* Message for the last non-OK status returned on this thread. */
 const char *rs_last_error(void);
 

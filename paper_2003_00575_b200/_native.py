@@ -8,15 +8,17 @@ present when a kernel is requested, calls raise ``RuntimeError``.
 from __future__ import annotations
 
 import ctypes
+import os
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "_lib" / "librangeseg_b200.so"
+LIB_PATH = Path(os.environ.get("RS_LIB") or
+                Path(__file__).resolve().parent / "_lib" / "librangeseg_b200.so")
 MAX_OFFSETS = 32
 
 RS_OK, RS_EINVAL, RS_ECUDA, RS_ETOOLARGE, RS_ENODEV = range(5)
 
 EXPORTS = ("rs_tables_count", "rs_plan", "rs_segment_batch", "rs_segment_batch_host",
-           "rs_stage_masks", "rs_last_error", "rs_version")
+           "rs_stage_masks", "rs_phase_profile", "rs_last_error", "rs_version")
 
 
 class RsConfig(ctypes.Structure):
@@ -59,6 +61,8 @@ def lib():
         L.rs_stage_masks.restype = ctypes.c_int
         L.rs_stage_masks.argtypes = [ctypes.POINTER(RsConfig), _P, _P, ctypes.c_int32,
                                      _P, _P, _P, _P]
+        L.rs_phase_profile.restype = ctypes.c_int
+        L.rs_phase_profile.argtypes = [_P, ctypes.c_int32]
         L.rs_last_error.restype = ctypes.c_char_p
         L.rs_version.restype = ctypes.c_int
         _lib = L

@@ -34,19 +34,26 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found")
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
+PROF_OUT = PKG / "_lib" / "librangeseg_b200_prof.so"
+
+
+def build(force: bool = False, verbose: bool = False, profile: bool = False) -> Path:
+    out = PROF_OUT if profile else OUT
     deps = [SRC, INCLUDE / "rangeseg_b200.h"]
-    if not force and OUT.exists() and all(OUT.stat().st_mtime >= d.stat().st_mtime for d in deps):
-        return OUT
-    OUT.parent.mkdir(parents=True, exist_ok=True)
-    tmp = OUT.with_suffix(".so.tmp")
+    if not force and out.exists() and all(out.stat().st_mtime >= d.stat().st_mtime for d in deps):
+        return out
+    out.parent.mkdir(parents=True, exist_ok=True)
+    tmp = out.with_suffix(".so.tmp")
     cmd = [nvcc(), *NVCC_FLAGS, "-I", str(INCLUDE), "-o", str(tmp), str(SRC)]
+    if profile:
+        cmd.insert(1, "-DRS_PHASE_PROF")
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     subprocess.run(cmd, check=True)
-    tmp.replace(OUT)
-    return OUT
+    tmp.replace(out)
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force=True, verbose=True))
+    import sys
+    print(build(force=True, verbose=True, profile="--profile" in sys.argv))

@@ -36,6 +36,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <climits>
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
@@ -69,18 +70,37 @@ struct KArgs {
     int32_t *ncl;
     int64_t *sizes;
     int64_t sizes_stride;
-    int H, W, R, C, SH;
+    int H, W, R, C, SH, WPR;      // WPR = 32-bit words per row (rows are word-aligned)
     int n_off;
     int dy[RS_MAX_OFFSETS];
     int dx[RS_MAX_OFFSETS];
     int min_points, ground;
     float dmax2, mount, keep_above, tch;
-    unsigned long long magicW;    // ceil(2^40 / W): exact i / W for i*W < 2^40
+    unsigned long long magicWPR;  // ceil(2^40 / WPR): exact w / WPR for w*WPR < 2^40
     // shared-memory layout, in 32-bit words
-    int o_P, o_L, o_U, o_Ph, o_Lh, o_seam, o_MC, o_TL, o_misc;
-    int nwords, hwords;
+    int o_P, o_L, o_U, o_SB, o_RS, o_Ph, o_Lh, o_seam, o_MC, o_TL;
+    int nwords;                   // R * WPR
     int use_tma;
 };
+
+constexpr uint32_t kFull = 0xffffffffu;
+
+// Optional per-phase timestamps (build with -DRS_PHASE_PROF; read back with
+// rs_phase_profile).  Compiled out otherwise.
+constexpr int kProfSlots = 16;
+constexpr int kProfCtas = 8192;
+#ifdef RS_PHASE_PROF
+__device__ long long g_prof[kProfCtas * kProfSlots];
+#define RS_MARK(i)                                                                  \
+    do {                                                                            \
+        if (threadIdx.x == 0 && blockIdx.x < kProfCtas)                             \
+            g_prof[blockIdx.x * kProfSlots + (i)] = clock64();                      \
+    } while (0)
+#else
+#define RS_MARK(i) \
+    do {           \
+    } while (0)
+#endif
 
 // ---------------------------------------------------------------- arithmetic
 
@@ -95,23 +115,17 @@ __device__ __forceinline__ bool pair_pass(float d1, float d2, float c, float thr
     return __fsub_rn(s, q) <= thr;
 }
 
-// Presence = valid && !ground for cell (r, c); `get(row, col)` returns the range.
-// ground.py:112-140 (pair k = max(r,1)-1; row 0 reuses pair 0 with its own
-// height) and range_image.py:125-127 (z = r*sin + mount, two roundings).
-template <class Get>
-__device__ __forceinline__ bool present_at(const KArgs &a, int r, int c, Get get) {
-    const float v = get(r, c);
-    const bool valid = v > 0.f;
-    if (!a.ground || !valid) return valid;
-    const int H = a.H;
-    const int k = (r >= 1 ? r : 1) - 1;
-    const float d1 = get(k, c);
-    const float d2 = get(k + 1, c);
+// Ground decision of a valid cell with range v in row r (ground.py:112-140 and
+// range_image.py:125-127): pair kk = max(r,1)-1 spans d1 (upper) and d2
+// (lower); row 0 reuses pair 0 with its own height.  Slope bounds are
+// multiplied through by the denominator, never divided.
+__device__ __forceinline__ bool is_ground(const KArgs &a, float d1, float d2, float v, int kk, int r) {
     const float *t = a.tables;
-    const float sa = __ldg(t + H + k);
-    const float ca = __ldg(t + 2 * H - 1 + k);
-    const float lo = __ldg(t + 3 * H - 2 + k);
-    const float hi = __ldg(t + 4 * H - 3 + k);
+    const int H = a.H;
+    const float sa = __ldg(t + H + kk);
+    const float ca = __ldg(t + 2 * H - 1 + kk);
+    const float lo = __ldg(t + 3 * H - 2 + kk);
+    const float hi = __ldg(t + 4 * H - 3 + kk);
     const float num = __fmul_rn(d2, sa);
     const float den = __fsub_rn(d1, __fmul_rn(d2, ca));
     const float L = __fmul_rn(lo, den);
@@ -119,16 +133,21 @@ __device__ __forceinline__ bool present_at(const KArgs &a, int r, int c, Get get
     bool ok = den > 0.f ? (num >= L && num <= U) : (num <= L && num >= U);
     ok = ok && den != 0.f && d1 > 0.f && d2 > 0.f;
     const float z = __fadd_rn(__fmul_rn(v, __ldg(t + r)), a.mount);
-    const bool low = z <= a.keep_above;
-    return !(ok && low);
+    return ok && z <= a.keep_above;
 }
 
-__device__ __forceinline__ unsigned divW(const KArgs &a, unsigned i) {
-    return (unsigned)(((unsigned long long)i * a.magicW) >> 40);
+// Presence = valid && !ground for cell (r, c); `get(row, col)` returns the range.
+template <class Get>
+__device__ __forceinline__ bool present_at(const KArgs &a, int r, int c, Get get) {
+    const float v = get(r, c);
+    if (!(v > 0.f)) return false;
+    if (!a.ground) return true;
+    const int kk = (r >= 1 ? r : 1) - 1;
+    return !is_ground(a, get(kk, c), get(kk + 1, c), v, kk, r);
 }
 
-__device__ __forceinline__ bool bit(const uint32_t *w, int i) {
-    return (w[i >> 5] >> (i & 31)) & 1u;
+__device__ __forceinline__ int divWPR(const KArgs &a, int w) {
+    return (int)(((unsigned long long)(unsigned)w * a.magicWPR) >> 40);
 }
 
 __device__ __forceinline__ uint32_t lanemask_le(int lane) {
@@ -175,12 +194,24 @@ __device__ __forceinline__ void tma_load_1d(void *dst, const void *src, uint32_t
 
 // ---------------------------------------------------------------- union-find
 //
-// Entries are cluster-encoded pixel indices e = (band << SH) | local, which
-// order exactly like frame-linear indices.  Invariant: E[e] <= e, so a root is
-// the minimum index of its tree.
+// Nodes are horizontal runs of linked cells inside a band, identified by the
+// local index of their first cell.  Entries hold cluster-encoded indices
+// e = (band << SH) | local, which order exactly like frame-linear indices.
+// Invariant: E[x] <= x (hooks point to the smaller root), so every tree's
+// root is its minimum cell.  Once roots are marked, a root's entry carries
+// kFlag | value (its size, later its label); finds treat kFlag as "root".
+
+
+// Node (local cell index) of cell bit b of word w: the last run start at or
+// before the cell, else the run node carried into the word.
+__device__ __forceinline__ uint32_t node_of(const uint32_t *SB, const uint32_t *RS, int w, int q, int cw,
+                                            int W, int b) {
+    const uint32_t s = SB[w] & lanemask_le(b);
+    return s ? (uint32_t)(q * W + cw * 32 + 31 - __clz(s)) : RS[w];
+}
 
 struct UF {
-    uint32_t *E;          // this CTA's entries (shared)
+    uint32_t *E;
     cg::cluster_group cl;
     uint32_t mask;
     int SH;
@@ -194,16 +225,26 @@ struct UF {
     __device__ __forceinline__ uint32_t ld(uint32_t e) const {
         return *reinterpret_cast<volatile uint32_t *>(slot(e));
     }
+    // find over the whole cluster (DSMEM), path halving, flag-aware
     __device__ uint32_t find(uint32_t e) const {
-        uint32_t p = ld(e);
-        while (p != e) {
+        while (true) {
+            const uint32_t p = ld(e);
+            if (p == e || (p & kFlag)) return e;
             const uint32_t gp = ld(p);
-            if (gp == p) return p;
-            *reinterpret_cast<volatile uint32_t *>(slot(e)) = gp;   // path halving
+            if (gp == p || (gp & kFlag)) return p;
+            *reinterpret_cast<volatile uint32_t *>(slot(e)) = gp;
             e = gp;
-            p = ld(e);
         }
-        return e;
+    }
+    // read-only find: used while owners overwrite their entries with final
+    // roots, where a late path-halving store could replace a root with an
+    // intermediate ancestor
+    __device__ uint32_t find_nc(uint32_t e) const {
+        while (true) {
+            const uint32_t p = ld(e);
+            if (p == e || (p & kFlag)) return e;
+            e = p;
+        }
     }
     __device__ void unite(uint32_t x, uint32_t y) const {
         while (true) {
@@ -211,7 +252,30 @@ struct UF {
             y = find(y);
             if (x == y) return;
             if (x > y) { const uint32_t t = x; x = y; y = t; }
-            const uint32_t old = atomicMin(slot(y), x);   // hook larger root under smaller
+            const uint32_t old = atomicMin(slot(y), x);
+            if (old == y) return;
+            y = old;
+        }
+    }
+    // band-local versions (all entries owned by this CTA): plain shared memory
+    __device__ uint32_t find_local(uint32_t e) const {
+        volatile uint32_t *V = E;
+        while (true) {
+            const uint32_t p = V[e & mask];
+            if (p == e) return e;
+            const uint32_t gp = V[p & mask];
+            if (gp == p) return p;
+            V[e & mask] = gp;
+            e = gp;
+        }
+    }
+    __device__ void unite_local(uint32_t x, uint32_t y) const {
+        while (true) {
+            x = find_local(x);
+            y = find_local(y);
+            if (x == y) return;
+            if (x > y) { const uint32_t t = x; x = y; y = t; }
+            const uint32_t old = atomicMin(E + (y & mask), x);
             if (old == y) return;
             y = old;
         }
@@ -224,342 +288,419 @@ __global__ void __launch_bounds__(kThreads, 2) rs_segment_kernel(const __grid_co
     extern __shared__ __align__(128) uint32_t sm[];
     __shared__ __align__(8) uint64_t mbar;
     __shared__ uint32_t warp_tot[kWarps];
-    __shared__ uint32_t cta_cnt, cta_sum, cta_prefix;
+    __shared__ uint32_t cta_cnt, cta_sum, cta_prefix, seam;
 
     cg::cluster_group cl = cg::this_cluster();
     const int k = (int)cl.block_rank();
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int frame = blockIdx.x / a.C;
-    const int H = a.H, W = a.W, R = a.R;
+    const int H = a.H, W = a.W, R = a.R, WPR = a.WPR;
     const int r0 = k * R;
     const int rows = min(R, H - r0);
-    const int n_own = rows * W;
-    const int n_pad = a.nwords * 32;
+    const int nw = rows * WPR;          // own words
     const float *fr = a.ranges + (size_t)frame * H * W;
     const int lo_row = max(r0 - 2, 0);
     const int hi_row = min(max(r0 + rows - 1, 1), H - 1);
-    const float thr = a.dmax2;
+    const float thr = a.dmax2, tch = a.tch;
     const uint32_t band = (uint32_t)k << a.SH;
 
     float *stage = reinterpret_cast<float *>(sm);
-    uint32_t *E = sm;   // aliases the staging area after the edge phase
+    uint32_t *E = sm;   // aliases the staging area once the edge bits exist
     uint32_t *P = sm + a.o_P, *L = sm + a.o_L, *U = sm + a.o_U;
-    uint32_t *Ph = sm + a.o_Ph, *Lh = sm + a.o_Lh, *seam = sm + a.o_seam;
+    uint32_t *SB = sm + a.o_SB, *RS = sm + a.o_RS;
+    uint32_t *Ph = sm + a.o_Ph, *Lh = sm + a.o_Lh;
     uint32_t *MC = sm + a.o_MC, *TL = sm + a.o_TL;
 
-    // ---- 1. stage rows [lo_row, hi_row] -------------------------------------
+    RS_MARK(0);
+    // ---- 1. stage rows [lo_row, hi_row] (TMA bulk copies) ---------------------
     const int n_stage = (hi_row - lo_row + 1) * W;
     const float *src = fr + (size_t)lo_row * W;
+    if (tid == 0) seam = 0;
     if (a.use_tma) {
         if (tid == 0) {
             mbar_init(&mbar, 1);
-            const uint32_t bytes = (uint32_t)n_stage * 4u;
-            mbar_expect_tx(&mbar, bytes);
+            mbar_expect_tx(&mbar, (uint32_t)n_stage * 4u);
             const uint32_t row_bytes = (uint32_t)W * 4u;
             for (int s = 0; s <= hi_row - lo_row; ++s)
                 tma_load_1d(stage + (size_t)s * W, src + (size_t)s * W, row_bytes, &mbar);
         }
-        if (tid < 32) seam[0] = 0;   // cleared while the copy is in flight
-        for (int i = tid; i < a.hwords; i += kThreads) { Ph[i] = 0; Lh[i] = 0; }
         __syncthreads();
         mbar_wait(&mbar, 0);
     } else {
         for (int i = tid; i < n_stage; i += kThreads) stage[i] = __ldg(src + i);
-        if (tid == 0) seam[0] = 0;
-        for (int i = tid; i < a.hwords; i += kThreads) { Ph[i] = 0; Lh[i] = 0; }
         __syncthreads();
     }
-
+    RS_MARK(1);
     auto S = [&](int r, int c) -> float { return stage[(r - lo_row) * W + c]; };
     auto G = [&](int r, int c) -> float { return __ldg(fr + (size_t)r * W + c); };
 
-    // ---- 2. presence bits: own rows, then the halo row r0-1 -----------------
-    for (int base = warp * 32; base < n_pad; base += kWarps * 32) {
-        const int i = base + lane;
-        bool p = false;
-        if (i < n_own) {
-            const int q = (int)divW(a, (unsigned)i);
-            p = present_at(a, r0 + q, i - q * W, S);
-        }
-        const uint32_t m = __ballot_sync(0xffffffffu, p);
-        if (lane == 0) P[base >> 5] = m;
-    }
-    if (r0 > 0) {
-        for (int base = warp * 32; base < a.hwords * 32; base += kWarps * 32) {
-            const int c = base + lane;
-            const bool p = c < W && present_at(a, r0 - 1, c, S);
-            const uint32_t m = __ballot_sync(0xffffffffu, p);
-            if (lane == 0) Ph[base >> 5] = m;
+    // ---- 2. presence, left and up edge bits -----------------------------------
+    // A warp walks a 32-column strip down the band, carrying the row above in
+    // registers; rows r0-1 (halo) .. r0+rows-1.  LEFT bit 0 of each word and
+    // the seam are completed in step 3.
+    {
+        const float *tcv = a.tables + 5 * H - 4;
+        const int rstart = r0 > 0 ? r0 - 1 : 0;
+        for (int cw = warp; cw < WPR; cw += kWarps) {
+            const int c = cw * 32 + lane;
+            const bool inb = c < W;
+            float vprev = (inb && rstart >= 1) ? S(rstart - 1, c) : 0.f;
+            bool pprev = false;
+            for (int r = rstart; r < r0 + rows; ++r) {
+                const float v = inb ? S(r, c) : 0.f;
+                bool p = v > 0.f;
+                if (a.ground && p) {
+                    const float d1 = r >= 1 ? vprev : v;
+                    const float d2 = r >= 1 ? v : S(1, c);
+                    p = !is_ground(a, d1, d2, v, r >= 1 ? r - 1 : 0, r);
+                }
+                const float vl = __shfl_up_sync(kFull, v, 1);
+                const bool pl = __shfl_up_sync(kFull, p, 1);
+                const bool left = lane > 0 && p && pl && pair_pass(vl, v, tch, thr);
+                const bool up = r > rstart && p && pprev && pair_pass(vprev, v, __ldg(tcv + r - 1), thr);
+                const uint32_t mp = __ballot_sync(kFull, p);
+                const uint32_t ml = __ballot_sync(kFull, left);
+                const uint32_t mu = __ballot_sync(kFull, up);
+                if (lane == 0) {
+                    if (r < r0) {
+                        Ph[cw] = mp;
+                        Lh[cw] = ml;
+                    } else {
+                        const int w = (r - r0) * WPR + cw;
+                        P[w] = mp;
+                        L[w] = ml;
+                        U[w] = mu;
+                    }
+                }
+                vprev = v;
+                pprev = p;
+            }
         }
     }
     __syncthreads();
 
-    // ---- 3. edge bits --------------------------------------------------------
-    // Halo row LEFT bits (needed by the cross-band redundant-edge test).
-    if (r0 > 0) {
-        for (int base = warp * 32; base < a.hwords * 32; base += kWarps * 32) {
-            const int c = base + lane;
-            bool l = false;
-            if (c > 0 && c < W && bit(Ph, c) && bit(Ph, c - 1))
-                l = pair_pass(S(r0 - 1, c - 1), S(r0 - 1, c), a.tch, thr);
-            const uint32_t m = __ballot_sync(0xffffffffu, l);
-            if (lane == 0) Lh[base >> 5] = m;
+    RS_MARK(2);
+    // ---- 3. word-boundary LEFT bits, the seam, Map Connection bits ------------
+    for (int w = tid; w < nw + WPR; w += kThreads) {
+        int cw, r;
+        uint32_t *Lw, pw, pprev;
+        if (w < nw) {
+            const int q = divWPR(a, w);
+            cw = w - q * WPR;
+            r = r0 + q;
+            if (cw == 0) continue;
+            Lw = L + w; pw = P[w]; pprev = P[w - 1];
+        } else {
+            if (r0 == 0) break;
+            cw = w - nw;
+            r = r0 - 1;
+            if (cw == 0) continue;
+            Lw = Lh + cw; pw = Ph[cw]; pprev = Ph[cw - 1];
+        }
+        const int c = cw * 32;
+        if ((pw & 1u) && (pprev >> 31) && pair_pass(S(r, c - 1), S(r, c), tch, thr)) *Lw |= 1u;
+    }
+    if (W > 1) {
+        for (int q = tid; q < rows; q += kThreads) {
+            const int r = r0 + q;
+            const uint32_t pe = P[q * WPR + (W - 1) / 32] >> ((W - 1) & 31);
+            if ((pe & 1u) && (P[q * WPR] & 1u) && pair_pass(S(r, W - 1), S(r, 0), tch, thr))
+                atomicOr(&seam, 1u << q);
         }
     }
-    const float *tcv = a.tables + 5 * H - 4;
-    for (int base = warp * 32; base < n_pad; base += kWarps * 32) {
-        const int i = base + lane;
-        const bool inb = i < n_own;
-        int q = 0, c = 0, r = r0;
-        if (inb) {
-            q = (int)divW(a, (unsigned)i);
-            c = i - q * W;
-            r = r0 + q;
-        }
-        const bool p = inb && bit(P, i);
-        const float v = inb ? S(r, c) : 0.f;
-        bool left = false, up = false;
-        if (p) {
-            if (c > 0) {
-                left = bit(P, i - 1) && pair_pass(S(r, c - 1), v, a.tch, thr);
-            } else if (W > 1) {
-                // seam edge (r, W-1) <-> (r, 0): horizontal[r, W-1] in the reference
-                if (bit(P, i + W - 1) && pair_pass(S(r, W - 1), v, a.tch, thr))
-                    atomicOr(seam, 1u << (q + 1));
-            }
-            if (r >= 1) {
-                const bool pu = (q == 0) ? bit(Ph, c) : bit(P, i - W);
-                up = pu && pair_pass(S(r - 1, c), v, __ldg(tcv + r - 1), thr);
-            }
-        }
-        const uint32_t ml = __ballot_sync(0xffffffffu, left);
-        const uint32_t mu = __ballot_sync(0xffffffffu, up);
-        if (lane == 0) {
-            L[base >> 5] = ml;
-            U[base >> 5] = mu;
-        }
-        // Map Connections, evaluated by the lower (or right) cell of each pair:
-        // partner t = (r - dy, (c - dx) mod W); TL = LEFT edge of t (for the
-        // redundant-edge test).
-        for (int o = 0; o < a.n_off; ++o) {
-            const int dy = a.dy[o], dx = a.dx[o];
-            const int tr = r - dy;
-            int tc = (c - dx) % W;
-            if (tc < 0) tc += W;
-            bool pt = false;
-            float vt = 0.f;
-            const bool has = inb && tr >= 0;
-            if (has) {
-                if (tr >= r0) {
-                    pt = bit(P, (tr - r0) * W + tc);
-                    vt = S(tr, tc);
-                } else if (tr == r0 - 1) {
-                    pt = bit(Ph, tc);
-                    vt = S(tr, tc);
-                } else {
-                    vt = G(tr, tc);
-                    pt = present_at(a, tr, tc, G);
+    if (a.n_off > 0) {
+        // Pairs (r-dy, c-dx mod W) <-> (r, c), evaluated by the lower/right cell.
+        // TL = LEFT edge of the partner (for the redundant-edge test in step 4).
+        for (int w = warp; w < nw; w += kWarps) {
+            const int q = divWPR(a, w);
+            const int cw = w - q * WPR;
+            const int c = cw * 32 + lane;
+            const bool inb = c < W;
+            const int r = r0 + q;
+            const bool p = inb && ((P[w] >> lane) & 1u);
+            const float v = inb ? S(r, c) : 0.f;
+            for (int o = 0; o < a.n_off; ++o) {
+                const int dy = a.dy[o], dx = a.dx[o];
+                const int tr = r - dy;
+                int tc = (c - dx) % W;
+                if (tc < 0) tc += W;
+                const bool has = inb && tr >= 0;
+                auto part = [&](int col, bool &pt, float &vt) {
+                    if (tr >= r0) {
+                        pt = (P[(tr - r0) * WPR + col / 32] >> (col & 31)) & 1u;
+                        vt = S(tr, col);
+                    } else if (tr == r0 - 1) {
+                        pt = (Ph[col / 32] >> (col & 31)) & 1u;
+                        vt = S(tr, col);
+                    } else {
+                        vt = G(tr, col);
+                        pt = present_at(a, tr, col, G);
+                    }
+                };
+                bool pt = false;
+                float vt = 0.f;
+                if (has) part(tc, pt, vt);
+                bool ptl = __shfl_up_sync(kFull, pt, 1);
+                float vtl = __shfl_up_sync(kFull, vt, 1);
+                if (has && tc > 0 && c > 0 && lane == 0) part(tc - 1, ptl, vtl);
+                const float tco = __ldg(a.tables + 6 * H - 5 + o * H + max(tr, 0));
+                const bool mc = has && p && pt && pair_pass(vt, v, tco, thr);
+                const bool tl = has && c > 0 && tc > 0 && pt && ptl && pair_pass(vtl, vt, tch, thr);
+                const uint32_t mm = __ballot_sync(kFull, mc);
+                const uint32_t mt = __ballot_sync(kFull, tl);
+                if (lane == 0) {
+                    MC[o * a.nwords + w] = mm;
+                    TL[o * a.nwords + w] = mt;
                 }
-            }
-            // partner's left neighbour: lane-1's partner when (c > 0, tc > 0)
-            bool ptl = __shfl_up_sync(0xffffffffu, pt, 1);
-            float vtl = __shfl_up_sync(0xffffffffu, vt, 1);
-            if (has && tc > 0 && c > 0 && lane == 0) {
-                const int tl = tc - 1;
-                if (tr >= r0) {
-                    ptl = bit(P, (tr - r0) * W + tl);
-                    vtl = S(tr, tl);
-                } else if (tr == r0 - 1) {
-                    ptl = bit(Ph, tl);
-                    vtl = S(tr, tl);
-                } else {
-                    vtl = G(tr, tl);
-                    ptl = present_at(a, tr, tl, G);
-                }
-            }
-            const float tco = __ldg(a.tables + 6 * H - 5 + o * H + max(tr, 0));
-            const bool mc = has && p && pt && pair_pass(vt, v, tco, thr);
-            const bool tl = has && c > 0 && tc > 0 && pt && ptl && pair_pass(vtl, vt, a.tch, thr);
-            const uint32_t mm = __ballot_sync(0xffffffffu, mc);
-            const uint32_t mt = __ballot_sync(0xffffffffu, tl);
-            if (lane == 0) {
-                MC[o * a.nwords + (base >> 5)] = mm;
-                TL[o * a.nwords + (base >> 5)] = mt;
             }
         }
     }
     __syncthreads();   // staging is dead from here on; E aliases it
 
-    // ---- 4. local union-find ---------------------------------------------
-    for (int base = warp * 32; base < n_pad; base += kWarps * 32) {
-        const int i = base + lane;
-        if (i < n_own) {
-            const uint32_t pw = P[base >> 5];
-            if (!((pw >> lane) & 1u)) {
-                E[i] = kFlag;
-            } else {
-                const uint32_t notl = ~L[base >> 5] & lanemask_le(lane);
-                const int j = notl ? 31 - __clz(notl) : 0;
-                E[i] = band | (uint32_t)(base + j);
+    RS_MARK(3);
+    UF uf{E, cl, (1u << a.SH) - 1u, a.SH, k};
+
+    // ---- 4. runs: start bits, carried run node per word, node init ----------
+    // Warp w owns the contiguous word range [wr0, wr1); a run continuing into
+    // the range gets a pseudo start at its first cell (united in step 5).
+    const int per = (nw + kWarps - 1) / kWarps;
+    const int wr0 = min(warp * per, nw), wr1 = min(wr0 + per, nw);
+    {
+        int carry = -1;
+        for (int cb = wr0; cb < wr1; cb += 32) {
+            const int w = cb + lane;
+            const bool act = w < wr1;
+            uint32_t sb = 0;
+            int base = 0;
+            if (act) {
+                const uint32_t pw = P[w], lw = L[w];
+                sb = pw & ~lw;
+                if (w == wr0 && (pw & lw & 1u)) sb |= 1u;
+                const int q = divWPR(a, w);
+                base = q * W + (w - q * WPR) * 32;
+            }
+            int inc = sb ? base + 31 - __clz(sb) : -1;
+            for (int off = 1; off < 32; off <<= 1) {
+                const int t = __shfl_up_sync(kFull, inc, off);
+                if (lane >= off) inc = max(inc, t);
+            }
+            inc = max(inc, carry);
+            int exc = __shfl_up_sync(kFull, inc, 1);
+            if (lane == 0) exc = carry;
+            if (act) {
+                SB[w] = sb;
+                RS[w] = (uint32_t)exc;
+                for (uint32_t m = sb; m; m &= m - 1) {
+                    const int s = base + __ffs(m) - 1;
+                    E[s] = band | (uint32_t)s;
+                }
+            }
+            carry = __shfl_sync(kFull, inc, 31);
+        }
+    }
+    __syncthreads();
+
+    RS_MARK(4);
+    // ---- 5. band-local unions -----------------------------------------------
+    // UP / Map Connection edges are skipped when the same pair of runs is
+    // already joined through the edge one cell to the left (both cells linked
+    // to their left neighbours and that neighbour pair has the same edge).
+    for (int w = tid; w < nw; w += kThreads) {
+        const int q = divWPR(a, w);
+        const int cw = w - q * WPR;
+        const uint32_t lw = L[w], sb = SB[w];
+        if (sb & lw & 1u)   // pseudo start: join the run it continues
+            uf.unite_local(band | node_of(SB, RS, w, q, cw, W, 0),
+                           band | node_of(SB, RS, w - 1, q, cw - 1, W, 31));
+        const uint32_t uw = U[w];
+        if (q > 0 && uw) {
+            const uint32_t uprev = (uw << 1) | (cw > 0 ? U[w - 1] >> 31 : 0u);
+            uint32_t nr = uw & ~(uprev & lw & L[w - WPR]);
+            for (; nr; nr &= nr - 1) {
+                const int b = __ffs(nr) - 1;
+                uf.unite_local(band | node_of(SB, RS, w, q, cw, W, b),
+                               band | node_of(SB, RS, w - WPR, q - 1, cw, W, b));
+            }
+        }
+        if (cw == 0 && ((seam >> q) & 1u))
+            uf.unite_local(band | node_of(SB, RS, w, q, 0, W, 0),
+                           band | node_of(SB, RS, q * WPR + (W - 1) / 32, q, (W - 1) / 32, W, (W - 1) & 31));
+        for (int o = 0; o < a.n_off; ++o) {
+            const int dy = a.dy[o];
+            if (q < dy) continue;   // partner above the band: step 7
+            const uint32_t *M = MC + o * a.nwords;
+            const uint32_t m = M[w];
+            if (!m) continue;
+            const uint32_t mprev = (m << 1) | (cw > 0 ? M[w - 1] >> 31 : 0u);
+            uint32_t nr = m & ~(mprev & lw & TL[o * a.nwords + w]);
+            for (; nr; nr &= nr - 1) {
+                const int b = __ffs(nr) - 1;
+                int tc = (cw * 32 + b - a.dx[o]) % W;
+                if (tc < 0) tc += W;
+                const int tq = q - dy;
+                uf.unite_local(band | node_of(SB, RS, w, q, cw, W, b),
+                               band | node_of(SB, RS, tq * WPR + tc / 32, tq, tc / 32, W, tc & 31));
             }
         }
     }
     __syncthreads();
-
-    UF uf{E, cl, (1u << a.SH) - 1u, a.SH, k};
-    const uint32_t seamw = seam[0];
-    for (int base = warp * 32; base < n_pad; base += kWarps * 32) {
-        const int i = base + lane;
-        if (i >= n_own) continue;
-        const int q = (int)divW(a, (unsigned)i);
-        const int c = i - q * W;
-        const bool l = bit(L, i);
-        if (lane == 0 && l) uf.unite(band | (uint32_t)(i - 1), band | (uint32_t)i);
-        if (q > 0 && bit(U, i)) {
-            const bool skip = c > 0 && l && bit(L, i - W) && bit(U, i - 1);
-            if (!skip) uf.unite(band | (uint32_t)i, band | (uint32_t)(i - W));
-        }
-        if (c == 0 && ((seamw >> (q + 1)) & 1u))
-            uf.unite(band | (uint32_t)(i + W - 1), band | (uint32_t)i);
-        for (int o = 0; o < a.n_off; ++o) {
-            const uint32_t *mcb = MC + o * a.nwords;
-            if (!bit(mcb, i)) continue;
-            const int tr = r0 + q - a.dy[o];
-            if (tr < r0) continue;   // cross-band: phase 5
-            const bool skip = c > 0 && l && bit(mcb, i - 1) && bit(TL + o * a.nwords, i);
-            if (skip) continue;
-            int tc = (c - a.dx[o]) % W;
-            if (tc < 0) tc += W;
-            uf.unite(band | (uint32_t)i, band | (uint32_t)((tr - r0) * W + tc));
+    RS_MARK(5);
+    // local flatten: every node points at its band-local root
+    for (int w = tid; w < nw; w += kThreads) {
+        const int q = divWPR(a, w);
+        const uint32_t base = (uint32_t)(q * W + (w - q * WPR) * 32);
+        for (uint32_t m = SB[w]; m; m &= m - 1) {
+            const uint32_t s = base + __ffs(m) - 1;
+            E[s] = uf.find_local(band | s);
         }
     }
-    __syncthreads();
-    for (int i = tid; i < n_own; i += kThreads) {
-        const uint32_t e = E[i];
-        if (!(e & kFlag)) E[i] = uf.find(e);
-    }
-    cl.sync();   // #1: every band's entries initialised and locally flat
+    cl.sync();   // #1: every band's runs are initialised and locally flat
 
-    // ---- 5. cross-band unions (DSMEM) -------------------------------------
+    RS_MARK(6);
+    // ---- 6. cross-band unions over DSMEM ----------------------------------
     if (r0 > 0) {
-        const uint32_t up_band = (uint32_t)(k - 1) << a.SH;
-        for (int c = tid; c < W; c += kThreads) {
-            if (!bit(U, c)) continue;
-            const bool skip = c > 0 && bit(L, c) && bit(Lh, c) && bit(U, c - 1);
-            if (!skip) uf.unite(band | (uint32_t)c, up_band | (uint32_t)((R - 1) * W + c));
+        const int ku = k - 1;
+        const uint32_t *SBu = cl.map_shared_rank(SB, ku), *RSu = cl.map_shared_rank(RS, ku);
+        const uint32_t bandu = (uint32_t)ku << a.SH;
+        for (int cw = tid; cw < WPR; cw += kThreads) {
+            const uint32_t uw = U[cw];
+            if (!uw) continue;
+            const uint32_t uprev = (uw << 1) | (cw > 0 ? U[cw - 1] >> 31 : 0u);
+            uint32_t nr = uw & ~(uprev & L[cw] & Lh[cw]);
+            const int wu = (R - 1) * WPR + cw;
+            for (; nr; nr &= nr - 1) {
+                const int b = __ffs(nr) - 1;
+                uf.unite(band | node_of(SB, RS, cw, 0, cw, W, b),
+                         bandu | node_of(SBu, RSu, wu, R - 1, cw, W, b));
+            }
         }
         for (int o = 0; o < a.n_off; ++o) {
             const int dy = a.dy[o];
-            const int lim = min(dy, rows) * W;   // rows q < dy have partners above r0
-            const uint32_t *mcb = MC + o * a.nwords;
-            for (int i = tid; i < lim; i += kThreads) {
-                if (!bit(mcb, i)) continue;
-                const int q = (int)divW(a, (unsigned)i);
-                const int c = i - q * W;
+            const uint32_t *M = MC + o * a.nwords;
+            const int lim = min(dy, rows) * WPR;
+            for (int w = tid; w < lim; w += kThreads) {
+                const uint32_t m = M[w];
+                if (!m) continue;
+                const int q = divWPR(a, w);
+                const int cw = w - q * WPR;
+                const uint32_t mprev = (m << 1) | (cw > 0 ? M[w - 1] >> 31 : 0u);
+                uint32_t nr = m & ~(mprev & L[w] & TL[o * a.nwords + w]);
                 const int tr = r0 + q - dy;
                 if (tr < 0) continue;
-                const bool skip = c > 0 && bit(L, i) && bit(mcb, i - 1) && bit(TL + o * a.nwords, i);
-                if (skip) continue;
-                int tc = (c - a.dx[o]) % W;
-                if (tc < 0) tc += W;
-                const int tk = tr / R;
-                uf.unite(band | (uint32_t)i, ((uint32_t)tk << a.SH) | (uint32_t)((tr - tk * R) * W + tc));
+                const int kt = tr / R, tq = tr - kt * R;
+                const uint32_t *SBt = cl.map_shared_rank(SB, kt), *RSt = cl.map_shared_rank(RS, kt);
+                for (; nr; nr &= nr - 1) {
+                    const int b = __ffs(nr) - 1;
+                    int tc = (cw * 32 + b - a.dx[o]) % W;
+                    if (tc < 0) tc += W;
+                    uf.unite(band | node_of(SB, RS, w, q, cw, W, b),
+                             ((uint32_t)kt << a.SH) |
+                                 node_of(SBt, RSt, tq * WPR + tc / 32, tq, tc / 32, W, tc & 31));
+                }
             }
         }
     }
     cl.sync();   // #2: the forest is final
 
-    // ---- 6a. resolve every pixel to its root (warp-aggregated chase) -------
-    for (int base = warp * 32; base < n_pad; base += kWarps * 32) {
-        const int i = base + lane;
-        const uint32_t e = i < n_own ? E[i] : kFlag;
-        const uint32_t prev = __shfl_up_sync(0xffffffffu, e, 1);
-        const bool head = (lane == 0) || (e != prev);
-        uint32_t g = e;
-        if (head && !(e & kFlag)) g = uf.find(e);
-        const uint32_t heads = __ballot_sync(0xffffffffu, head);
-        const int hl = 31 - __clz(heads & lanemask_le(lane));
-        g = __shfl_sync(0xffffffffu, g, hl);
-        if (i < n_own && !(e & kFlag)) E[i] = g;
+    RS_MARK(7);
+    // ---- 7. resolve every node to its root; roots start a size counter ------
+    for (int w = tid; w < nw; w += kThreads) {
+        const int q = divWPR(a, w);
+        const uint32_t base = (uint32_t)(q * W + (w - q * WPR) * 32);
+        for (uint32_t m = SB[w]; m; m &= m - 1) {
+            const uint32_t s = base + __ffs(m) - 1;
+            const uint32_t g = uf.find_nc(band | s);
+            E[s] = g == (band | s) ? kFlag : g;
+        }
     }
     cl.sync();   // #3
 
-    // ---- 6b. mark roots (size counters start at 0) -------------------------
-    for (int i = tid; i < n_own; i += kThreads)
-        if (E[i] == (band | (uint32_t)i)) E[i] = kFlag;
+    RS_MARK(8);
+    // ---- 8. component sizes: one atomicAdd of the run length per run -------
+    {
+        int carry = INT_MAX;   // first run end after the current chunk
+        const int nchunks = (wr1 - wr0 + 31) / 32;
+        for (int ci = nchunks - 1; ci >= 0; --ci) {
+            const int w = wr0 + ci * 32 + lane;
+            const bool act = w < wr1;
+            uint32_t eb = 0, sb = 0;
+            int base = 0;
+            if (act) {
+                const int q = divWPR(a, w);
+                const int cw = w - q * WPR;
+                base = q * W + cw * 32;
+                const uint32_t lnext = (w + 1 < wr1 && cw + 1 < WPR) ? (L[w + 1] & 1u) : 0u;
+                eb = P[w] & ~((L[w] >> 1) | (lnext << 31));
+                sb = SB[w];
+            }
+            int inc = eb ? base + __ffs(eb) - 1 : INT_MAX;
+            for (int off = 1; off < 32; off <<= 1) {
+                const int t = __shfl_down_sync(kFull, inc, off);
+                if (lane + off < 32) inc = min(inc, t);
+            }
+            inc = min(inc, carry);
+            int exc = __shfl_down_sync(kFull, inc, 1);
+            if (lane == 31) exc = carry;
+            for (uint32_t m = sb; m; m &= m - 1) {
+                const int b = __ffs(m) - 1;
+                const uint32_t after = eb & ~((1u << b) - 1u);
+                const int end = after ? base + __ffs(after) - 1 : exc;
+                const uint32_t s = (uint32_t)(base + b);
+                const uint32_t v = E[s];
+                const uint32_t root = (v & kFlag) ? (band | s) : v;
+                atomicAdd(uf.slot(root), (uint32_t)(end - (int)s + 1));
+            }
+            carry = __shfl_sync(kFull, inc, 0);
+        }
+    }
     cl.sync();   // #4
 
-    // ---- 6c. component sizes ----------------------------------------------
-    for (int base = warp * 32; base < n_pad; base += kWarps * 32) {
-        const int i = base + lane;
-        const bool p = i < n_own && bit(P, i);
-        uint32_t root = 0xffffffffu;
-        if (p) {
-            const uint32_t v = E[i];
-            root = (v & kFlag) ? (band | (uint32_t)i) : v;
-        }
-        const uint32_t prev = __shfl_up_sync(0xffffffffu, root, 1);
-        const bool head = (lane == 0) || (root != prev);
-        const uint32_t heads = __ballot_sync(0xffffffffu, head);
-        if (head && p) {
-            const uint32_t after = heads & ~lanemask_le(lane);
-            const int next = after ? __ffs(after) - 1 : 32;
-            atomicAdd(uf.slot(root), (uint32_t)(next - lane));
-        }
-    }
-    cl.sync();   // #5
-
-    // ---- 6d. kept roots, ordered scan, labels for roots ---------------------
-    uint32_t *K = U;    // reuse: U/L bits are dead after the unions
+    RS_MARK(9);
+    // ---- 9. filter + ordered rank of kept roots ---------------------------
+    uint32_t *K = U;    // U and L are dead after the unions and sizes
     uint32_t *WP = L;
     const uint32_t minp = a.min_points > 1 ? (uint32_t)a.min_points : 1u;
-    if (tid == 0) { cta_cnt = 0; cta_sum = 0; }
+    if (tid == 0) cta_sum = 0;
     __syncthreads();
-    for (int base = warp * 32; base < n_pad; base += kWarps * 32) {
-        const int i = base + lane;
-        bool kept = false;
-        uint32_t sz = 0;
-        if (i < n_own && bit(P, i)) {
-            const uint32_t v = E[i];
-            if (v & kFlag) {
-                sz = v & ~kFlag;
-                kept = sz >= minp;
+    for (int w = tid; w < nw; w += kThreads) {
+        const int q = divWPR(a, w);
+        const uint32_t base = (uint32_t)(q * W + (w - q * WPR) * 32);
+        uint32_t kept = 0, s_sum = 0;
+        for (uint32_t m = SB[w]; m; m &= m - 1) {
+            const int b = __ffs(m) - 1;
+            const uint32_t v = E[base + b];
+            if ((v & kFlag) && (v & ~kFlag) >= minp) {
+                kept |= 1u << b;
+                s_sum += v & ~kFlag;
             }
         }
-        const uint32_t m = __ballot_sync(0xffffffffu, kept);
-        uint32_t s = kept ? sz : 0u;
-        for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-        if (lane == 0) {
-            K[base >> 5] = m;
-            if (s) atomicAdd(&cta_sum, s);
-        }
+        K[w] = kept;
+        if (s_sum) atomicAdd(&cta_sum, s_sum);
     }
     __syncthreads();
-    // word-ordered exclusive scan: warp w owns words [w*per, (w+1)*per)
-    const int per = (a.nwords + kWarps - 1) / kWarps;
     {
         uint32_t run = 0;
-        const int w0 = warp * per, w1 = min(w0 + per, a.nwords);
-        for (int cb = w0; cb < w1; cb += 32) {
+        for (int cb = wr0; cb < wr1; cb += 32) {
             const int w = cb + lane;
-            const uint32_t cnt = w < w1 ? __popc(K[w]) : 0u;
+            const uint32_t cnt = w < wr1 ? __popc(K[w]) : 0u;
             uint32_t inc = cnt;
             for (int off = 1; off < 32; off <<= 1) {
-                const uint32_t t = __shfl_up_sync(0xffffffffu, inc, off);
+                const uint32_t t = __shfl_up_sync(kFull, inc, off);
                 if (lane >= off) inc += t;
             }
-            if (w < w1) WP[w] = run + inc - cnt;
-            run += __shfl_sync(0xffffffffu, inc, 31);
+            if (w < wr1) WP[w] = run + inc - cnt;
+            run += __shfl_sync(kFull, inc, 31);
         }
         if (lane == 0) warp_tot[warp] = run;
     }
     __syncthreads();
     if (tid == 0) {
         uint32_t t = 0;
-        for (int w = 0; w < kWarps; ++w) { const uint32_t x = warp_tot[w]; warp_tot[w] = t; t += x; }
+        for (int i = 0; i < kWarps; ++i) { const uint32_t x = warp_tot[i]; warp_tot[i] = t; t += x; }
         cta_cnt = t;
     }
-    cl.sync();   // #6: every band's count and kept-size sum are published
+    cl.sync();   // #5: every band's kept count and kept-size sum are published
+    RS_MARK(10);
     if (tid == 0) {
         uint32_t pre = 0, tot = 0, sum = 0;
         for (int j = 0; j < a.C; ++j) {
@@ -575,40 +716,57 @@ __global__ void __launch_bounds__(kThreads, 2) rs_segment_kernel(const __grid_co
         }
     }
     __syncthreads();
-    const uint32_t prefix = cta_prefix;
-    for (int base = warp * 32; base < n_pad; base += kWarps * 32) {
-        const int i = base + lane;
-        if (i >= n_own || !bit(P, i)) continue;
-        const uint32_t v = E[i];
-        if (!(v & kFlag)) continue;
-        const int w = base >> 5;
-        const uint32_t km = K[w];
-        if ((km >> lane) & 1u) {
-            const uint32_t label = prefix + warp_tot[w / per] + WP[w] +
-                                   __popc(km & (lanemask_le(lane) >> 1)) + 1u;
-            E[i] = kFlag | label;
-            if (a.sizes) a.sizes[(size_t)frame * a.sizes_stride + label] = (int64_t)(v & ~kFlag);
-        } else {
-            E[i] = kFlag;   // dropped by filter_small
+    {
+        const uint32_t prefix = cta_prefix;
+        for (int w = tid; w < nw; w += kThreads) {
+            const int q = divWPR(a, w);
+            const uint32_t base = (uint32_t)(q * W + (w - q * WPR) * 32);
+            const uint32_t km = K[w];
+            const uint32_t wbase = prefix + warp_tot[min(w / max(per, 1), kWarps - 1)] + WP[w];
+            for (uint32_t m = SB[w]; m; m &= m - 1) {
+                const int b = __ffs(m) - 1;
+                const uint32_t s = base + b;
+                const uint32_t v = E[s];
+                if (!(v & kFlag)) continue;
+                if ((km >> b) & 1u) {
+                    const uint32_t label = wbase + __popc(km & ((1u << b) - 1u)) + 1u;
+                    E[s] = kFlag | label;
+                    if (a.sizes) a.sizes[(size_t)frame * a.sizes_stride + label] = (int64_t)(v & ~kFlag);
+                } else {
+                    E[s] = kFlag;   // dropped by filter_small
+                }
+            }
         }
     }
-    cl.sync();   // #7
+    cl.sync();   // #6
 
-    // ---- 7. labels --------------------------------------------------------
-    int32_t *out = a.labels + (size_t)frame * H * W + (size_t)r0 * W;
-    for (int base = warp * 32; base < n_pad; base += kWarps * 32) {
-        const int i = base + lane;
-        const uint32_t v = i < n_own ? E[i] : kFlag;
-        const uint32_t prev = __shfl_up_sync(0xffffffffu, v, 1);
-        const bool head = (lane == 0) || (v != prev);
-        uint32_t lab = v & ~kFlag;
-        if (head && !(v & kFlag)) lab = uf.ld(v) & ~kFlag;
-        const uint32_t heads = __ballot_sync(0xffffffffu, head);
-        const int hl = 31 - __clz(heads & lanemask_le(lane));
-        lab = __shfl_sync(0xffffffffu, lab, hl);
-        if (i < n_own) __stcs(out + i, (int32_t)lab);
+    RS_MARK(11);
+    // ---- 10. every node takes its root's label -----------------------------
+    for (int w = tid; w < nw; w += kThreads) {
+        const int q = divWPR(a, w);
+        const uint32_t base = (uint32_t)(q * W + (w - q * WPR) * 32);
+        for (uint32_t m = SB[w]; m; m &= m - 1) {
+            const uint32_t s = base + __ffs(m) - 1;
+            const uint32_t v = E[s];
+            if (!(v & kFlag)) E[s] = kFlag | (uf.ld(v) & ~kFlag);
+        }
     }
-    cl.sync();   // #8: no CTA leaves while its shared memory may still be read
+    cl.sync();   // #7: no DSMEM access after this point
+
+    RS_MARK(12);
+    // ---- 11. per-cell labels, coalesced streaming stores -------------------
+    int32_t *out = a.labels + (size_t)frame * H * W + (size_t)r0 * W;
+    for (int w = warp; w < nw; w += kWarps) {
+        const int q = divWPR(a, w);
+        const int cw = w - q * WPR;
+        const int c = cw * 32 + lane;
+        if (c < W) {
+            uint32_t lab = 0;
+            if ((P[w] >> lane) & 1u) lab = E[node_of(SB, RS, w, q, cw, W, lane)] & ~kFlag;
+            __stcs(out + q * W + c, (int32_t)lab);
+        }
+    }
+    RS_MARK(13);
 }
 
 // Stage masks (parity/debug): ground, horizontal, vertical as bytes.
@@ -668,19 +826,20 @@ int validate(const rs_config *cfg) {
 }
 
 size_t smem_for(int R, int W, int n_off, int *o_words) {
-    const int nwords = (R * W + 31) / 32;
-    const int hwords = (W + 31) / 32;
-    const int stage = (R + 2) * W;
+    const int WPR = (W + 31) / 32;
+    const int nwords = R * WPR;
+    const int stage = std::max((R + 2) * W, R * W);
     int off = (stage + 31) & ~31;
     o_words[0] = off; off += nwords;               // P
     o_words[1] = off; off += nwords;               // L
     o_words[2] = off; off += nwords;               // U
-    o_words[3] = off; off += hwords;               // Ph
-    o_words[4] = off; off += hwords;               // Lh
-    o_words[5] = off; off += 1;                    // seam
-    o_words[6] = off; off += n_off * nwords;       // MC
-    o_words[7] = off; off += n_off * nwords;       // TL
-    o_words[8] = off;
+    o_words[3] = off; off += nwords;               // SB (run starts)
+    o_words[4] = off; off += nwords;               // RS (run node carried into a word)
+    o_words[5] = off; off += WPR;                  // Ph (halo row)
+    o_words[6] = off; off += WPR;                  // Lh
+    o_words[7] = off; off += 0;                    // (seam lives in static smem)
+    o_words[8] = off; off += n_off * nwords;       // MC
+    o_words[9] = off; off += n_off * nwords;       // TL
     return (size_t)off * 4u;
 }
 
@@ -688,7 +847,7 @@ int make_plan(const rs_config *cfg, Plan *pl) {
     int st = validate(cfg);
     if (st) return st;
     const int H = cfg->height, W = cfg->width, n_off = cfg->n_offsets;
-    int o[9];
+    int o[10];
     int R = cfg->rows_per_cta;
     if (R <= 0) {
         // Prefer ~16K cells per CTA (two CTAs per SM) with a portable cluster.
@@ -725,11 +884,11 @@ int make_plan(const rs_config *cfg, Plan *pl) {
     k.mount = cfg->mount_height;
     k.keep_above = cfg->keep_above;
     k.tch = cfg->two_cos_h;
-    k.magicW = ((1ULL << 40) + (unsigned long long)W - 1) / (unsigned long long)W;
-    k.o_P = o[0]; k.o_L = o[1]; k.o_U = o[2]; k.o_Ph = o[3]; k.o_Lh = o[4]; k.o_seam = o[5];
-    k.o_MC = o[6]; k.o_TL = o[7]; k.o_misc = o[8];
-    k.nwords = (R * W + 31) / 32;
-    k.hwords = (W + 31) / 32;
+    k.WPR = (W + 31) / 32;
+    k.magicWPR = ((1ULL << 40) + (unsigned long long)k.WPR - 1) / (unsigned long long)k.WPR;
+    k.o_P = o[0]; k.o_L = o[1]; k.o_U = o[2]; k.o_SB = o[3]; k.o_RS = o[4];
+    k.o_Ph = o[5]; k.o_Lh = o[6]; k.o_seam = o[7]; k.o_MC = o[8]; k.o_TL = o[9];
+    k.nwords = R * k.WPR;
     return RS_OK;
 }
 
@@ -952,6 +1111,19 @@ int rs_segment_batch_host(const rs_config *cfg, const float *h_tables, const flo
     const int st1 = cuda_check(cudaStreamSynchronize(g_host.s[1]), "stream sync");
     cudaEventDestroy(tables_ready);
     return st ? st : (st0 ? st0 : st1);
+}
+
+int rs_phase_profile(int64_t *host_out, int32_t max_ctas) {
+#ifdef RS_PHASE_PROF
+    const int n = std::min<int>(max_ctas, kProfCtas);
+    if (!host_out || n <= 0) return fail(RS_EINVAL, "bad profile buffer");
+    return cuda_check(cudaMemcpyFromSymbol(host_out, g_prof, (size_t)n * kProfSlots * sizeof(long long)),
+                      "read phase profile");
+#else
+    (void)host_out;
+    (void)max_ctas;
+    return fail(RS_EINVAL, "library built without RS_PHASE_PROF");
+#endif
 }
 
 const char *rs_last_error(void) { return g_err.c_str(); }

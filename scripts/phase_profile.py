@@ -1,0 +1,47 @@
+"""Per-phase CTA timing from the RS_PHASE_PROF build (clock64 deltas)."""
+import argparse
+import ctypes
+import os
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+os.environ["RS_LIB"] = str(ROOT / "paper_2003_00575_b200" / "_lib" / "librangeseg_b200_prof.so")
+sys.path.insert(0, str(ROOT))
+
+import numpy as np
+import torch
+
+import paper_2003_00575_b200 as rs
+from paper_2003_00575_b200 import _native, synthetic
+
+p = argparse.ArgumentParser()
+p.add_argument("--config", type=int, default=1)
+p.add_argument("--batch", type=int, default=256)
+p.add_argument("--core", action="store_true")
+p.add_argument("--skip", type=int, default=0)
+p.add_argument("--rows", type=int, default=0)
+a = p.parse_args()
+names = ["stage", "bitsA", "bitsB/MC", "runs", "local-union", "flatten+cs1", "cross+cs2",
+         "resolve+cs3", "sizes+cs4", "kept+scan+cs5", "assign+cs6", "nodelabel+cs7", "labels"]
+spec = synthetic.CONFIGS[a.config]
+frames = synthetic.make_batch(a.config, a.batch, device="cuda")
+cfg = (rs.PipelineConfig(mc_pattern=rs.skip_pattern(a.skip), ground_removal=False, min_cluster_points=1)
+       if a.core else rs.PipelineConfig(mc_pattern=rs.skip_pattern(a.skip)))
+pipe = rs.Pipeline(synthetic.sensor_for(spec), cfg, rows_per_cta=a.rows)
+for _ in range(3):
+    pipe.segment_batch(frames)
+torch.cuda.synchronize()
+ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+ev[0].record(); pipe.segment_batch(frames); ev[1].record(); torch.cuda.synchronize()
+n = min(8192, a.batch * pipe.ctas_per_frame)
+buf = np.zeros((n, 16), dtype=np.int64)
+_native.check(_native.lib().rs_phase_profile(buf.ctypes.data_as(ctypes.c_void_p), n))
+d = np.diff(buf[:, :14], axis=1).astype(np.float64)
+tot = buf[:, 13] - buf[:, 0]
+print(f"kernel {ev[0].elapsed_time(ev[1])*1e3:.1f} us, plan R={pipe.rows_per_cta} C={pipe.ctas_per_frame} "
+      f"smem={pipe.smem_bytes}, CTAs profiled {n}")
+print(f"CTA lifetime cycles: mean {tot.mean():.0f} p50 {np.median(tot):.0f} p90 {np.percentile(tot,90):.0f}")
+for i, nm in enumerate(names):
+    print(f"  {nm:16s} mean {d[:, i].mean():9.0f}  p90 {np.percentile(d[:, i], 90):9.0f}  "
+          f"share {100*d[:, i].mean()/tot.mean():5.1f}%")

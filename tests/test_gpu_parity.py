@@ -177,7 +177,7 @@ def test_serpentine_component(cuda):
         f[r + 1, (W - 1) if (r // 2) % 2 == 0 else 0] = 5.0 if r + 1 < H else 0
     f[:, 1::17] = 0.0
     cfg = rs.PipelineConfig(ground_removal=False, min_cluster_points=1)
-    for rows in (1, 4, 8):
+    for rows in (4, 8, 16):
         pipe, res = _run(model, cfg, f, rows_per_cta=rows)
         wl, ws = oracle.segment_frame(f, pipe.packed)
         _assert_frame(res, 0, wl, ws)
