@@ -64,7 +64,7 @@ typedef struct rs_config {
     float keep_above;                       /* f32(GroundParams.resolve_keep_above) */
     float two_cos_h;                        /* f32(pair_constant(0, 1)) */
     int32_t rows_per_cta;                   /* 0 = automatic band height */
-    int32_t reserved[3];
+    int32_t reserved[3];                    /* [0]: node-capacity cap (tests); else 0 */
 } rs_config;
 
 /* Number of floats in the constant-table block. */
@@ -75,11 +75,22 @@ size_t rs_tables_count(int32_t height, int32_t n_offsets);
 int rs_plan(const rs_config *cfg, int32_t *rows_per_cta, int32_t *ctas_per_frame,
             size_t *smem_bytes);
 
+/* Plan details: {fast kernel used, overflow possible, fast rows, fast CTAs,
+ * fast smem, node capacity, dense rows, dense CTAs, dense smem}. */
+int rs_plan_detail(const rs_config *cfg, int32_t *out, int32_t n);
+
+/* Device workspace rs_segment_batch needs for `batch` frames (the overflow
+ * list of frames handed from the fast to the dense kernel).  Zero it once
+ * after allocation; the library leaves it zeroed after every call.  One
+ * workspace per stream. */
+size_t rs_workspace_size(const rs_config *cfg, int32_t batch);
+
 /* B frames, device pointers, enqueued on `stream` (a cudaStream_t; NULL = legacy
- * default stream).  Asynchronous: returns after the launch. */
+ * default stream).  Asynchronous: returns after the launch(es). */
 int rs_segment_batch(const rs_config *cfg, const float *d_tables, const float *d_ranges,
                      int32_t batch, int32_t *d_labels, int32_t *d_n_clusters,
-                     int64_t *d_cluster_sizes, int64_t sizes_stride, void *stream);
+                     int64_t *d_cluster_sizes, int64_t sizes_stride,
+                     void *d_workspace, size_t workspace_size, void *stream);
 
 /* Same on host buffers (pinned memory gives overlapped copies).  Synchronous. */
 int rs_segment_batch_host(const rs_config *cfg, const float *h_tables, const float *h_ranges,

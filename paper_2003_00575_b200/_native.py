@@ -17,8 +17,9 @@ MAX_OFFSETS = 32
 
 RS_OK, RS_EINVAL, RS_ECUDA, RS_ETOOLARGE, RS_ENODEV = range(5)
 
-EXPORTS = ("rs_tables_count", "rs_plan", "rs_segment_batch", "rs_segment_batch_host",
-           "rs_stage_masks", "rs_phase_profile", "rs_last_error", "rs_version")
+EXPORTS = ("rs_tables_count", "rs_plan", "rs_plan_detail", "rs_workspace_size",
+           "rs_segment_batch", "rs_segment_batch_host", "rs_stage_masks", "rs_phase_profile",
+           "rs_last_error", "rs_version")
 
 
 class RsConfig(ctypes.Structure):
@@ -54,7 +55,12 @@ def lib():
                               ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_size_t)]
         L.rs_segment_batch.restype = ctypes.c_int
         L.rs_segment_batch.argtypes = [ctypes.POINTER(RsConfig), _P, _P, ctypes.c_int32,
-                                       _P, _P, _P, ctypes.c_int64, _P]
+                                       _P, _P, _P, ctypes.c_int64, _P, ctypes.c_size_t, _P]
+        L.rs_plan_detail.restype = ctypes.c_int
+        L.rs_plan_detail.argtypes = [ctypes.POINTER(RsConfig), ctypes.POINTER(ctypes.c_int32),
+                                     ctypes.c_int32]
+        L.rs_workspace_size.restype = ctypes.c_size_t
+        L.rs_workspace_size.argtypes = [ctypes.POINTER(RsConfig), ctypes.c_int32]
         L.rs_segment_batch_host.restype = ctypes.c_int
         L.rs_segment_batch_host.argtypes = [ctypes.POINTER(RsConfig), _P, _P, ctypes.c_int32,
                                             _P, _P, _P, ctypes.c_int64]
@@ -79,7 +85,7 @@ def check(status: int, what: str = "rangeseg_b200"):
     raise RuntimeError(f"{what}: {msg}")
 
 
-def make_config(packed, rows_per_cta: int = 0) -> RsConfig:
+def make_config(packed, rows_per_cta: int = 0, node_capacity: int = 0) -> RsConfig:
     if len(packed.offsets) > MAX_OFFSETS:
         raise ValueError(f"at most {MAX_OFFSETS} Map Connection offsets are supported")
     cfg = RsConfig()
@@ -94,7 +100,18 @@ def make_config(packed, rows_per_cta: int = 0) -> RsConfig:
     cfg.keep_above = float(packed.keep_above)
     cfg.two_cos_h = float(packed.two_cos_h)
     cfg.rows_per_cta = int(rows_per_cta)
+    cfg.reserved[0] = int(node_capacity)
     return cfg
+
+
+PLAN_FIELDS = ("fast", "may_overflow", "fast_rows", "fast_ctas", "fast_smem", "node_capacity",
+               "dense_rows", "dense_ctas", "dense_smem")
+
+
+def plan_detail(cfg: RsConfig) -> dict:
+    out = (ctypes.c_int32 * len(PLAN_FIELDS))()
+    check(lib().rs_plan_detail(ctypes.byref(cfg), out, len(PLAN_FIELDS)), "rs_plan_detail")
+    return dict(zip(PLAN_FIELDS, list(out)))
 
 
 def plan(cfg: RsConfig):

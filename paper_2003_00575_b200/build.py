@@ -16,6 +16,7 @@ from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
 SRC = PKG / "csrc" / "rangeseg_b200.cu"
+HEADERS = sorted((PKG / "csrc").glob("*.cuh"))
 OUT = PKG / "_lib" / "librangeseg_b200.so"
 INCLUDE = PKG.parent / "include"
 
@@ -39,7 +40,7 @@ PROF_OUT = PKG / "_lib" / "librangeseg_b200_prof.so"
 
 def build(force: bool = False, verbose: bool = False, profile: bool = False) -> Path:
     out = PROF_OUT if profile else OUT
-    deps = [SRC, INCLUDE / "rangeseg_b200.h"]
+    deps = [SRC, INCLUDE / "rangeseg_b200.h", *HEADERS]
     if not force and out.exists() and all(out.stat().st_mtime >= d.stat().st_mtime for d in deps):
         return out
     out.parent.mkdir(parents=True, exist_ok=True)

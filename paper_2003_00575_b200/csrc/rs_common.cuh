@@ -1,0 +1,177 @@
+// rs_common.cuh — shared device code: kernel arguments, the float32 decision
+// rules of the reference, bit helpers, TMA/mbarrier wrappers, phase markers.
+#pragma once
+
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include <climits>
+#include <cstdint>
+
+#include "../../include/rangeseg_b200.h"
+
+namespace cg = cooperative_groups;
+
+namespace rs {
+
+constexpr uint32_t kFull = 0xffffffffu;
+constexpr uint32_t kFlag = 0x80000000u;
+
+struct KArgs {
+    const float *ranges;
+    const float *tables;
+    int32_t *labels;
+    int32_t *ncl;
+    int64_t *sizes;
+    int64_t sizes_stride;
+    int H, W, R, C, SH, WPR;      // WPR = 32-bit words per row (rows are word-aligned)
+    int n_off;
+    int dy[RS_MAX_OFFSETS];
+    int dx[RS_MAX_OFFSETS];
+    int min_points, ground;
+    float dmax2, mount, keep_above, tch;
+    unsigned long long magicWPR;  // ceil(2^40 / WPR): exact w / WPR for w*WPR < 2^40
+    int nwords;                   // R * WPR
+    // shared-memory layout (32-bit words); meaning depends on the kernel
+    int o_P, o_L, o_U, o_SB, o_RS, o_Ph, o_Lh, o_MC, o_TL, o_LR, o_K, o_E, o_SZ;
+    int NC, SHN;                  // fast kernel: run-node capacity per band, id bits
+    int use_tma;                  // dense kernel: stage rows with TMA bulk copies
+    int *ws;                      // [0] overflow count, [1] done counter, [2..] frame list
+    int list_mode;                // dense kernel: process the overflow list
+};
+
+// ------------------------------------------------------------ phase markers
+constexpr int kProfSlots = 16;
+constexpr int kProfCtas = 8192;
+#ifdef RS_PHASE_PROF
+__device__ long long g_prof[kProfCtas * kProfSlots];
+#define RS_MARK(i)                                                             \
+    do {                                                                       \
+        if (threadIdx.x == 0 && blockIdx.x < kProfCtas)                        \
+            ::rs::g_prof[blockIdx.x * kProfSlots + (i)] = clock64();           \
+    } while (0)
+#else
+#define RS_MARK(i) \
+    do {           \
+    } while (0)
+#endif
+
+// ---------------------------------------------------------------- arithmetic
+
+// pair_distance_sq (connectivity.py:54) compared with d_max_sq: five separately
+// rounded float32 ops.  The >=0 clamp (:55) cannot change the decision.
+__device__ __forceinline__ bool pair_pass(float d1, float d2, float c, float thr) {
+    const float a = __fmul_rn(d1, d1);
+    const float b = __fmul_rn(d2, d2);
+    const float s = __fadd_rn(a, b);
+    const float p = __fmul_rn(d1, d2);
+    const float q = __fmul_rn(c, p);
+    return __fsub_rn(s, q) <= thr;
+}
+
+// Row constants of the ground rule for cell row r (pair kk = max(r,1)-1).
+struct GroundRow {
+    float sa, ca, lo, hi, sc;
+};
+
+__device__ __forceinline__ GroundRow ground_row(const KArgs &a, int r) {
+    const float *t = a.tables;
+    const int H = a.H;
+    const int kk = (r >= 1 ? r : 1) - 1;
+    GroundRow g;
+    g.sa = __ldg(t + H + kk);
+    g.ca = __ldg(t + 2 * H - 1 + kk);
+    g.lo = __ldg(t + 3 * H - 2 + kk);
+    g.hi = __ldg(t + 4 * H - 3 + kk);
+    g.sc = __ldg(t + r);
+    return g;
+}
+
+// Ground decision of a valid cell with range v (ground.py:112-140,
+// range_image.py:125-127): d1/d2 are the upper/lower ranges of the row's
+// pair.  The tangent bounds are multiplied through by the denominator (never
+// divided), with the interval flipped when it is negative.
+__device__ __forceinline__ bool ground_rule(const KArgs &a, const GroundRow &g, float d1, float d2, float v) {
+    const float num = __fmul_rn(d2, g.sa);
+    const float den = __fsub_rn(d1, __fmul_rn(d2, g.ca));
+    const float L = __fmul_rn(g.lo, den);
+    const float U = __fmul_rn(g.hi, den);
+    const bool okp = num >= L && num <= U;
+    const bool okn = num <= L && num >= U;
+    const bool ok = (den > 0.f ? okp : okn) && den != 0.f && d1 > 0.f && d2 > 0.f;
+    const float z = __fadd_rn(__fmul_rn(v, g.sc), a.mount);
+    return ok && z <= a.keep_above;
+}
+
+// The same decision with the row constants in registers and the window test
+// as min(L,U) <= num <= max(L,U): lo <= hi and rounding is monotone, so
+// [L, U] is ordered for den > 0 and reversed for den < 0 — exactly the
+// reference's two branches; den == 0 fails either way.
+__device__ __forceinline__ bool ground_rule_mm(const KArgs &a, float sa, float ca, float lo, float hi,
+                                               float sc, float d1, float d2, float v) {
+    const float num = __fmul_rn(d2, sa);
+    const float den = __fsub_rn(d1, __fmul_rn(d2, ca));
+    const float L = __fmul_rn(lo, den);
+    const float U = __fmul_rn(hi, den);
+    const bool ok = fminf(L, U) <= num && num <= fmaxf(L, U) && den != 0.f && fminf(d1, d2) > 0.f;
+    const float z = __fadd_rn(__fmul_rn(v, sc), a.mount);
+    return ok && z <= a.keep_above;
+}
+
+// Presence = valid && !ground for cell (r, c); `get(row, col)` returns the range.
+template <class Get>
+__device__ __forceinline__ bool present_at(const KArgs &a, int r, int c, Get get) {
+    const float v = get(r, c);
+    if (!(v > 0.f)) return false;
+    if (!a.ground) return true;
+    const int kk = (r >= 1 ? r : 1) - 1;
+    return !ground_rule(a, ground_row(a, r), get(kk, c), get(kk + 1, c), v);
+}
+
+__device__ __forceinline__ int divWPR(const KArgs &a, int w) {
+    return (int)(((unsigned long long)(unsigned)w * a.magicWPR) >> 40);
+}
+
+__device__ __forceinline__ uint32_t lanemask_le(int lane) {
+    return lane == 31 ? 0xffffffffu : ((2u << lane) - 1u);
+}
+
+// ------------------------------------------------------------- TMA staging
+
+__device__ __forceinline__ uint32_t smem_addr(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(smem_addr(bar)), "r"(phase)
+            : "memory");
+    }
+}
+
+__device__ __forceinline__ void tma_load_1d(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_addr(dst)),
+        "l"(src), "r"(bytes), "r"(smem_addr(bar))
+        : "memory");
+}
+
+}  // namespace rs

@@ -1,0 +1,640 @@
+// rs_fast.cuh — the fast kernel: union-find over compactly numbered runs.
+//
+// One thread-block cluster per frame, one 256-thread CTA per band of R rows
+// spanning the full width (so the azimuth seam is CTA-local).  Shared memory
+// holds only bit planes and per-run state, so four CTAs share an SM:
+//
+//   A  presence / left / up edge bits straight from global memory: each warp
+//      walks 32-column strips down the band, keeping the row above in
+//      registers and prefetching two rows ahead (the reference's float32
+//      rules, one rounding per op: ground.py:112-140, connectivity.py:47-92).
+//   B  word-boundary left bits, the seam, Map Connection bits.
+//   R  runs: start bits, and a block scan of their counts that numbers the
+//      runs of the band 0..n-1 in cell order (run id order == cell order).
+//   U  band-local union-find over run ids in shared memory (atomicMin hooks,
+//      redundant-edge skipping), local flatten, local component sizes.
+//   X  cross-band unions over DSMEM, one thread per boundary column.
+//   Z  every local root resolves its global root (read-only chase) and adds
+//      its local size there; other runs resolve through their local root.
+//   K  kept roots (size >= min_points), ordered scan over run ids, cluster
+//      prefix -> label = 1 + rank of the component's first cell among kept
+//      components, which is the reference's first-encounter numbering after
+//      _renumber_roots and filter_small (SURVEY.md finding 2).
+//   L  run labels, then per-cell labels with 16-byte streaming stores.
+//
+// A band with more runs than the node capacity NC marks the frame; the whole
+// cluster then leaves and the frame is appended to the overflow list, which
+// rs_dense_kernel processes right after (stream-ordered).
+#pragma once
+
+#include "rs_common.cuh"
+
+namespace rs {
+
+constexpr int kFastThreads = 256;
+constexpr int kFastWarps = kFastThreads / 32;
+
+// Run id of cell bit b of word w: runs started at or before the cell in this
+// word, plus the runs started before the word.
+__device__ __forceinline__ uint32_t run_of(const uint32_t *SB, const uint32_t *NB, int w, int b) {
+    return NB[w] + __popc(SB[w] & lanemask_le(b)) - 1u;
+}
+
+struct RunUF {
+    uint32_t *E;
+    cg::cluster_group cl;
+    uint32_t mask;
+    int SHN;
+    int rank;
+
+    __device__ __forceinline__ uint32_t *slot(uint32_t *arr, uint32_t e) const {
+        const int owner = (int)(e >> SHN);
+        return (owner == rank ? arr : cl.map_shared_rank(arr, owner)) + (e & mask);
+    }
+    __device__ __forceinline__ uint32_t ld(uint32_t e) const {
+        return *reinterpret_cast<volatile uint32_t *>(slot(E, e));
+    }
+    __device__ uint32_t find(uint32_t e) const {
+        while (true) {
+            const uint32_t p = ld(e);
+            if (p == e) return e;
+            const uint32_t gp = ld(p);
+            if (gp == p) return p;
+            *reinterpret_cast<volatile uint32_t *>(slot(E, e)) = gp;   // path halving
+            e = gp;
+        }
+    }
+    __device__ uint32_t find_nc(uint32_t e) const {   // read-only
+        while (true) {
+            const uint32_t p = ld(e);
+            if (p == e) return e;
+            e = p;
+        }
+    }
+    __device__ void unite(uint32_t x, uint32_t y) const {
+        while (true) {
+            x = find(x);
+            y = find(y);
+            if (x == y) return;
+            if (x > y) { const uint32_t t = x; x = y; y = t; }
+            const uint32_t old = atomicMin(slot(E, y), x);   // larger root hooks under smaller
+            if (old == y) return;
+            y = old;
+        }
+    }
+    __device__ uint32_t find_local(uint32_t e) const {
+        volatile uint32_t *V = E;
+        while (true) {
+            const uint32_t p = V[e & mask];
+            if (p == e) return e;
+            const uint32_t gp = V[p & mask];
+            if (gp == p) return p;
+            V[e & mask] = gp;
+            e = gp;
+        }
+    }
+    __device__ void unite_local(uint32_t x, uint32_t y) const {
+        while (true) {
+            x = find_local(x);
+            y = find_local(y);
+            if (x == y) return;
+            if (x > y) { const uint32_t t = x; x = y; y = t; }
+            const uint32_t old = atomicMin(E + (y & mask), x);
+            if (old == y) return;
+            y = old;
+        }
+    }
+};
+
+__global__ void __launch_bounds__(kFastThreads, 4) rs_fast_kernel(const __grid_constant__ KArgs a) {
+    extern __shared__ __align__(128) uint32_t sm[];
+    __shared__ uint32_t warp_tot[kFastWarps];
+    __shared__ uint32_t cta_cnt, cta_sum, cta_prefix, seam, ovf, ovf_any;
+    __shared__ __align__(16) float rowc[(32 + 1) * 8];   // per-row constants of the band
+
+    cg::cluster_group cl = cg::this_cluster();
+    const int k = (int)cl.block_rank();
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int frame = blockIdx.x / a.C;
+    const int H = a.H, W = a.W, R = a.R, WPR = a.WPR;
+    const int r0 = k * R;
+    const int rows = min(R, H - r0);
+    const int nw = rows * WPR;
+    const float *fr = a.ranges + (size_t)frame * H * W;
+    const float thr = a.dmax2, tch = a.tch;
+    const uint32_t band = (uint32_t)k << a.SHN;
+    const uint32_t maskN = (1u << a.SHN) - 1u;
+
+    uint32_t *P = sm + a.o_P, *L = sm + a.o_L, *U = sm + a.o_U;
+    uint32_t *SB = sm + a.o_SB, *NB = sm + a.o_RS;
+    uint32_t *Ph = sm + a.o_Ph, *Lh = sm + a.o_Lh;
+    uint32_t *MC = sm + a.o_MC, *TL = sm + a.o_TL;
+    uint32_t *LR = sm + a.o_LR, *KB = sm + a.o_K;
+    uint32_t *E = sm + a.o_E, *SZ = sm + a.o_SZ;
+    auto G = [&](int r, int c) -> float { return __ldg(fr + (size_t)r * W + c); };
+
+    RS_MARK(0);
+    if (tid == 0) { seam = 0; cta_sum = 0; }
+
+    // ---- A. presence, left and up bits --------------------------------------
+    // Row constants of the band (ground pair, height sine, vertical 2cos)
+    // are staged once; each lane then handles 4 consecutive cells of a
+    // 128-column chunk and walks down the rows with the row above in
+    // registers.  Nibbles are gathered into 32-bit words with a 3-step OR
+    // butterfly over the 8 lanes of a word.
+    const int rstart = r0 > 0 ? r0 - 1 : 0;
+    const int rend = r0 + rows;
+    for (int r = rstart + tid; r < rend; r += kFastThreads) {
+        const GroundRow g = ground_row(a, r);
+        float *rc = rowc + (r - rstart) * 8;
+        rc[0] = g.sa; rc[1] = g.ca; rc[2] = g.lo; rc[3] = g.hi; rc[4] = g.sc;
+        rc[5] = r >= 1 ? __ldg(a.tables + 5 * H - 4 + r - 1) : 0.f;
+    }
+    __syncthreads();
+    {
+        const bool vec = (W & 3) == 0;
+        const int nchunk = (W + 127) / 128;
+        for (int ch = warp; ch < nchunk; ch += kFastWarps) {
+            const int c0 = ch * 128 + lane * 4;
+            auto ld4 = [&](int r) -> float4 {
+                const float *rowp = fr + (size_t)r * W;
+                if (vec && c0 + 3 < W) return __ldg(reinterpret_cast<const float4 *>(rowp + c0));
+                float4 x;
+                x.x = c0 < W ? __ldg(rowp + c0) : 0.f;
+                x.y = c0 + 1 < W ? __ldg(rowp + c0 + 1) : 0.f;
+                x.z = c0 + 2 < W ? __ldg(rowp + c0 + 2) : 0.f;
+                x.w = c0 + 3 < W ? __ldg(rowp + c0 + 3) : 0.f;
+                return x;
+            };
+            float4 vprev = rstart >= 1 ? ld4(rstart - 1) : make_float4(0.f, 0.f, 0.f, 0.f);
+            float4 v = ld4(rstart);
+            float4 vnext = ld4(rstart + 1);   // H >= 2; row 0 needs row 1 for its ground pair
+            uint32_t pprev = 0;
+            for (int r = rstart; r < rend; ++r) {
+                const float4 vn2 = (r + 2 < rend) ? ld4(r + 2) : make_float4(0.f, 0.f, 0.f, 0.f);
+                const float4 c = *reinterpret_cast<const float4 *>(rowc + (r - rstart) * 8);
+                const float2 c2 = *reinterpret_cast<const float2 *>(rowc + (r - rstart) * 8 + 4);
+                const float vv[4] = {v.x, v.y, v.z, v.w};
+                const float va[4] = {vprev.x, vprev.y, vprev.z, vprev.w};
+                const float vb[4] = {vnext.x, vnext.y, vnext.z, vnext.w};
+                uint32_t np = 0;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const float d1 = r >= 1 ? va[j] : vv[j];
+                    const float d2 = r >= 1 ? vv[j] : vb[j];
+                    bool p = vv[j] > 0.f;
+                    if (a.ground) p = p && !ground_rule_mm(a, c.x, c.y, c.z, c.w, c2.x, d1, d2, vv[j]);
+                    np |= (uint32_t)p << j;
+                }
+                // left neighbour of cell j is cell j-1; cell 0 takes lane-1's cell 3
+                const float vl = __shfl_up_sync(kFull, v.w, 1);
+                const uint32_t npl = __shfl_up_sync(kFull, np, 1);
+                uint32_t nl = 0, nu = 0;
+                if (lane > 0 && (np & 1u) && (npl & 8u) && pair_pass(vl, vv[0], tch, thr)) nl |= 1u;
+#pragma unroll
+                for (int j = 1; j < 4; ++j)
+                    if (((np >> j) & 1u) && ((np >> (j - 1)) & 1u) && pair_pass(vv[j - 1], vv[j], tch, thr))
+                        nl |= 1u << j;
+                if (r > rstart) {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+                        if (((np & pprev) >> j) & 1u && pair_pass(va[j], vv[j], c2.y, thr)) nu |= 1u << j;
+                }
+                const int sh = (lane & 7) * 4;
+                uint32_t xp = np << sh, xl = nl << sh, xu = nu << sh;
+#pragma unroll
+                for (int m = 1; m < 8; m <<= 1) {
+                    xp |= __shfl_xor_sync(kFull, xp, m);
+                    xl |= __shfl_xor_sync(kFull, xl, m);
+                    xu |= __shfl_xor_sync(kFull, xu, m);
+                }
+                const int cw = ch * 4 + (lane >> 3);
+                if ((lane & 7) == 0 && cw < WPR) {
+                    if (r < r0) {
+                        Ph[cw] = xp;
+                        Lh[cw] = xl;
+                    } else {
+                        const int w = (r - r0) * WPR + cw;
+                        P[w] = xp;
+                        L[w] = xl;
+                        U[w] = xu;
+                    }
+                }
+                vprev = v;
+                v = vnext;
+                vnext = vn2;
+                pprev = np;
+            }
+        }
+    }
+    __syncthreads();
+    RS_MARK(1);
+
+    // ---- B. word-boundary left bits, seam, Map Connection bits ---------------
+    for (int w = tid; w < nw + WPR; w += kFastThreads) {
+        int cw, r;
+        uint32_t *Lw, pw, pprev;
+        if (w < nw) {
+            const int q = divWPR(a, w);
+            cw = w - q * WPR;
+            r = r0 + q;
+            if ((cw & 3) != 0 || cw == 0) continue;   // set in A except at chunk starts
+            Lw = L + w; pw = P[w]; pprev = P[w - 1];
+        } else {
+            if (r0 == 0) break;
+            cw = w - nw;
+            r = r0 - 1;
+            if ((cw & 3) != 0 || cw == 0) continue;
+            Lw = Lh + cw; pw = Ph[cw]; pprev = Ph[cw - 1];
+        }
+        const int c = cw * 32;
+        if ((pw & 1u) && (pprev >> 31) && pair_pass(G(r, c - 1), G(r, c), tch, thr)) *Lw |= 1u;
+    }
+    if (W > 1) {
+        for (int q = tid; q < rows; q += kFastThreads) {
+            const int r = r0 + q;
+            const uint32_t pe = P[q * WPR + (W - 1) / 32] >> ((W - 1) & 31);
+            if ((pe & 1u) && (P[q * WPR] & 1u) && pair_pass(G(r, W - 1), G(r, 0), tch, thr))
+                atomicOr(&seam, 1u << q);
+        }
+    }
+    if (a.n_off > 0) {
+        // Pairs (r-dy, c-dx mod W) <-> (r, c), evaluated by the lower/right cell;
+        // TL = left edge of the partner (redundant-edge test).
+        for (int w = warp; w < nw; w += kFastWarps) {
+            const int q = divWPR(a, w);
+            const int cw = w - q * WPR;
+            const int c = cw * 32 + lane;
+            const bool inb = c < W;
+            const int r = r0 + q;
+            const bool p = inb && ((P[w] >> lane) & 1u);
+            const float v = inb ? G(r, c) : 0.f;
+            for (int o = 0; o < a.n_off; ++o) {
+                const int tr = r - a.dy[o];
+                int tc = (c - a.dx[o]) % W;
+                if (tc < 0) tc += W;
+                const bool has = inb && tr >= 0;
+                auto part = [&](int col, bool &pt, float &vt) {
+                    vt = G(tr, col);
+                    if (tr >= r0)
+                        pt = (P[(tr - r0) * WPR + col / 32] >> (col & 31)) & 1u;
+                    else if (tr == r0 - 1)
+                        pt = (Ph[col / 32] >> (col & 31)) & 1u;
+                    else
+                        pt = present_at(a, tr, col, G);
+                };
+                bool pt = false;
+                float vt = 0.f;
+                if (has) part(tc, pt, vt);
+                bool ptl = __shfl_up_sync(kFull, pt, 1);
+                float vtl = __shfl_up_sync(kFull, vt, 1);
+                if (has && tc > 0 && c > 0 && lane == 0) part(tc - 1, ptl, vtl);
+                const float tco = __ldg(a.tables + 6 * H - 5 + o * H + max(tr, 0));
+                const bool mc = has && p && pt && pair_pass(vt, v, tco, thr);
+                const bool tl = has && c > 0 && tc > 0 && pt && ptl && pair_pass(vtl, vt, tch, thr);
+                const uint32_t mm = __ballot_sync(kFull, mc);
+                const uint32_t mt = __ballot_sync(kFull, tl);
+                if (lane == 0) {
+                    MC[o * a.nwords + w] = mm;
+                    TL[o * a.nwords + w] = mt;
+                }
+            }
+        }
+    }
+    __syncthreads();
+    RS_MARK(2);
+
+    // ---- R. runs and their ids ------------------------------------------------
+    // Warp `warp` owns words [wr0, wr1); a run continuing into the range gets a
+    // pseudo start at its first cell (joined to its run in step U).
+    const int per = (nw + kFastWarps - 1) / kFastWarps;
+    const int wr0 = min(warp * per, nw), wr1 = min(wr0 + per, nw);
+    {
+        uint32_t run = 0;
+        for (int cb = wr0; cb < wr1; cb += 32) {
+            const int w = cb + lane;
+            uint32_t sb = 0;
+            if (w < wr1) {
+                const uint32_t pw = P[w], lw = L[w];
+                sb = (pw & ~lw) | ((w == wr0) ? (pw & lw & 1u) : 0u);
+            }
+            const uint32_t cnt = __popc(sb);
+            uint32_t inc = cnt;
+            for (int off = 1; off < 32; off <<= 1) {
+                const uint32_t t = __shfl_up_sync(kFull, inc, off);
+                if (lane >= off) inc += t;
+            }
+            if (w < wr1) {
+                SB[w] = sb;
+                NB[w] = run + inc - cnt;
+            }
+            run += __shfl_sync(kFull, inc, 31);
+        }
+        if (lane == 0) warp_tot[warp] = run;
+    }
+    __syncthreads();
+    uint32_t n_runs = 0, my_off = 0;
+    for (int i = 0; i < kFastWarps; ++i) {
+        if (i < warp) my_off += warp_tot[i];
+        n_runs += warp_tot[i];
+    }
+    if (tid == 0) ovf = n_runs > (uint32_t)a.NC;
+    const bool overflow = n_runs > (uint32_t)a.NC;   // block-uniform
+    if (!overflow) {
+        for (int w = wr0 + lane; w < wr1; w += 32) NB[w] += my_off;
+        for (uint32_t id = tid; id < n_runs; id += kFastThreads) {
+            E[id] = band | id;
+            SZ[id] = 0;
+        }
+    }
+    __syncthreads();
+    RS_MARK(3);
+
+    RunUF uf{E, cl, maskN, a.SHN, k};
+    const uint32_t seamw = seam;
+    if (!overflow) {
+        // ---- U. band-local unions ----------------------------------------------
+        for (int w = tid; w < nw; w += kFastThreads) {
+            const int q = divWPR(a, w);
+            const int cw = w - q * WPR;
+            const uint32_t lw = L[w], sb = SB[w];
+            if (sb & lw & 1u)   // pseudo start: join the run it continues
+                uf.unite_local(band | run_of(SB, NB, w, 0), band | run_of(SB, NB, w - 1, 31));
+            const uint32_t uw = U[w];
+            if (q > 0 && uw) {
+                const uint32_t uprev = (uw << 1) | (cw > 0 ? U[w - 1] >> 31 : 0u);
+                for (uint32_t nr = uw & ~(uprev & lw & L[w - WPR]); nr; nr &= nr - 1) {
+                    const int b = __ffs(nr) - 1;
+                    uf.unite_local(band | run_of(SB, NB, w, b), band | run_of(SB, NB, w - WPR, b));
+                }
+            }
+            if (cw == 0 && ((seamw >> q) & 1u))
+                uf.unite_local(band | run_of(SB, NB, w, 0),
+                               band | run_of(SB, NB, q * WPR + (W - 1) / 32, (W - 1) & 31));
+            for (int o = 0; o < a.n_off; ++o) {
+                const int dy = a.dy[o];
+                if (q < dy) continue;   // partner above the band: step X
+                const uint32_t *M = MC + o * a.nwords;
+                const uint32_t m = M[w];
+                if (!m) continue;
+                const uint32_t mprev = (m << 1) | (cw > 0 ? M[w - 1] >> 31 : 0u);
+                for (uint32_t nr = m & ~(mprev & lw & TL[o * a.nwords + w]); nr; nr &= nr - 1) {
+                    const int b = __ffs(nr) - 1;
+                    int tc = (cw * 32 + b - a.dx[o]) % W;
+                    if (tc < 0) tc += W;
+                    uf.unite_local(band | run_of(SB, NB, w, b),
+                                   band | run_of(SB, NB, (q - dy) * WPR + tc / 32, tc & 31));
+                }
+            }
+        }
+        __syncthreads();
+        // local flatten; LR marks the band-local roots
+        for (uint32_t base = warp * 32; base < n_runs; base += kFastThreads) {
+            const uint32_t id = base + lane;
+            bool lr = false;
+            if (id < n_runs) {
+                // read-only chase: a concurrent path-halving store could
+                // otherwise replace a finished root pointer by an ancestor
+                const volatile uint32_t *V = E;
+                uint32_t r = band | id;
+                for (uint32_t p = V[r & maskN]; p != r; p = V[r & maskN]) r = p;
+                E[id] = r;
+                lr = r == (band | id);
+            }
+            const uint32_t m = __ballot_sync(kFull, lr);
+            if (lane == 0) LR[base >> 5] = m;
+        }
+        __syncthreads();
+        // local component sizes: each run adds its length to its local root
+        int carry = INT_MAX;   // first run end after the current chunk
+        const int nchunks = (wr1 - wr0 + 31) / 32;
+        for (int ci = nchunks - 1; ci >= 0; --ci) {
+            const int w = wr0 + ci * 32 + lane;
+            const bool act = w < wr1;
+            uint32_t eb = 0, sb = 0;
+            int base = 0;
+            if (act) {
+                const int q = divWPR(a, w);
+                const int cw = w - q * WPR;
+                base = q * W + cw * 32;
+                const uint32_t lnext = (w + 1 < wr1 && cw + 1 < WPR) ? (L[w + 1] & 1u) : 0u;
+                eb = P[w] & ~((L[w] >> 1) | (lnext << 31));
+                sb = SB[w];
+            }
+            int inc = eb ? base + __ffs(eb) - 1 : INT_MAX;
+            for (int off = 1; off < 32; off <<= 1) {
+                const int t = __shfl_down_sync(kFull, inc, off);
+                if (lane + off < 32) inc = min(inc, t);
+            }
+            inc = min(inc, carry);
+            int exc = __shfl_down_sync(kFull, inc, 1);
+            if (lane == 31) exc = carry;
+            if (sb) {
+                uint32_t id = NB[w];
+                for (uint32_t m = sb; m; m &= m - 1, ++id) {
+                    const int b = __ffs(m) - 1;
+                    const uint32_t after = eb & ~((1u << b) - 1u);
+                    const int end = after ? base + __ffs(after) - 1 : exc;
+                    atomicAdd(SZ + (E[id] & maskN), (uint32_t)(end - (base + b) + 1));
+                }
+            }
+            carry = __shfl_sync(kFull, inc, 0);
+        }
+    }
+    RS_MARK(4);
+    cl.sync();   // #1: every band's runs are numbered, joined locally and sized
+
+    if (tid == 0) {
+        uint32_t any = 0;
+        for (int j = 0; j < a.C; ++j) any |= *cl.map_shared_rank(&ovf, j);
+        ovf_any = any;
+    }
+    __syncthreads();
+    if (ovf_any) {   // cluster-uniform: the dense kernel takes this frame
+        if (k == 0 && tid == 0) a.ws[2 + atomicAdd(a.ws, 1)] = frame;
+        cl.sync();
+        return;
+    }
+
+    // ---- X. cross-band unions (DSMEM), one thread per boundary column --------
+    if (r0 > 0) {
+        const int ku = k - 1;
+        const uint32_t *SBu = cl.map_shared_rank(SB, ku), *NBu = cl.map_shared_rank(NB, ku);
+        const uint32_t bandu = (uint32_t)ku << a.SHN;
+        const int wu0 = (R - 1) * WPR;
+        for (int c = tid; c < W; c += kFastThreads) {
+            const int cw = c >> 5, b = c & 31;
+            const uint32_t uw = U[cw];
+            if (!((uw >> b) & 1u)) continue;
+            const uint32_t upb = b > 0 ? (uw >> (b - 1)) & 1u : (cw > 0 ? U[cw - 1] >> 31 : 0u);
+            if (upb && ((L[cw] >> b) & 1u) && ((Lh[cw] >> b) & 1u)) continue;   // redundant
+            uf.unite(band | run_of(SB, NB, cw, b), bandu | run_of(SBu, NBu, wu0 + cw, b));
+        }
+        for (int o = 0; o < a.n_off; ++o) {
+            const int dy = a.dy[o];
+            const uint32_t *M = MC + o * a.nwords, *T = TL + o * a.nwords;
+            for (int q = 0; q < min(dy, rows); ++q) {
+                const int tr = r0 + q - dy;
+                if (tr < 0) continue;
+                const int kt = tr / R, tq = tr - kt * R;
+                const uint32_t *SBt = cl.map_shared_rank(SB, kt), *NBt = cl.map_shared_rank(NB, kt);
+                for (int c = tid; c < W; c += kFastThreads) {
+                    const int cw = c >> 5, b = c & 31, w = q * WPR + cw;
+                    const uint32_t m = M[w];
+                    if (!((m >> b) & 1u)) continue;
+                    const uint32_t mpb = b > 0 ? (m >> (b - 1)) & 1u : (cw > 0 ? M[w - 1] >> 31 : 0u);
+                    if (mpb && ((L[w] >> b) & 1u) && ((T[w] >> b) & 1u)) continue;
+                    int tc = (c - a.dx[o]) % W;
+                    if (tc < 0) tc += W;
+                    uf.unite(band | run_of(SB, NB, w, b),
+                             ((uint32_t)kt << a.SHN) | run_of(SBt, NBt, tq * WPR + tc / 32, tc & 31));
+                }
+            }
+        }
+    }
+    RS_MARK(5);
+    cl.sync();   // #2: the forest is final
+
+    // ---- Z. resolve: local roots chase their global root and add their size ---
+    for (uint32_t id = tid; id < n_runs; id += kFastThreads) {
+        if (!((LR[id >> 5] >> (id & 31)) & 1u)) continue;
+        const uint32_t g = uf.find_nc(band | id);
+        if (g != (band | id)) {
+            E[id] = g;
+            atomicAdd(uf.slot(SZ, g), SZ[id]);
+        }
+    }
+    __syncthreads();
+    for (uint32_t id = tid; id < n_runs; id += kFastThreads) {
+        if ((LR[id >> 5] >> (id & 31)) & 1u) continue;
+        const uint32_t p = E[id];
+        E[id] = ((p >> a.SHN) == (uint32_t)k) ? E[p & maskN] : uf.find_nc(p);
+    }
+    RS_MARK(6);
+    cl.sync();   // #3: sizes are final at every root
+
+    // ---- K. kept roots, ordered rank ------------------------------------------
+    const uint32_t minp = a.min_points > 1 ? (uint32_t)a.min_points : 1u;
+    const uint32_t nkw = (n_runs + 31) / 32;
+    for (uint32_t base = warp * 32; base < nkw * 32; base += kFastThreads) {
+        const uint32_t id = base + lane;
+        bool kept = false;
+        uint32_t s = 0;
+        if (id < n_runs && E[id] == (band | id)) {
+            s = SZ[id];
+            kept = s >= minp;
+        }
+        const uint32_t m = __ballot_sync(kFull, kept);
+        s = kept ? s : 0u;
+        for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(kFull, s, off);
+        if (lane == 0) {
+            KB[base >> 5] = m;
+            if (s) atomicAdd(&cta_sum, s);
+        }
+    }
+    __syncthreads();
+    {
+        // block exclusive scan of popc(KB[w]) in word order; WK reuses LR
+        uint32_t *WK = LR;
+        uint32_t run = 0;
+        const uint32_t wper = (nkw + kFastWarps - 1) / kFastWarps;
+        const uint32_t w0 = min(warp * wper, nkw), w1 = min(w0 + wper, nkw);
+        for (uint32_t cb = w0; cb < w1; cb += 32) {
+            const uint32_t w = cb + lane;
+            const uint32_t cnt = w < w1 ? __popc(KB[w]) : 0u;
+            uint32_t inc = cnt;
+            for (int off = 1; off < 32; off <<= 1) {
+                const uint32_t t = __shfl_up_sync(kFull, inc, off);
+                if (lane >= off) inc += t;
+            }
+            if (w < w1) WK[w] = run + inc - cnt;
+            run += __shfl_sync(kFull, inc, 31);
+        }
+        if (lane == 0) warp_tot[warp] = run;
+        __syncthreads();
+        if (tid == 0) {
+            uint32_t t = 0;
+            for (int i = 0; i < kFastWarps; ++i) { const uint32_t x = warp_tot[i]; warp_tot[i] = t; t += x; }
+            cta_cnt = t;
+        }
+        __syncthreads();
+        for (uint32_t w = tid; w < nkw; w += kFastThreads)
+            WK[w] += warp_tot[min(w / max(wper, 1u), (uint32_t)kFastWarps - 1)];
+    }
+    RS_MARK(7);
+    cl.sync();   // #4: every band's kept count and kept-size sum are published
+    if (tid == 0) {
+        uint32_t pre = 0, tot = 0, sum = 0;
+        for (int j = 0; j < a.C; ++j) {
+            const uint32_t cj = *cl.map_shared_rank(&cta_cnt, j);
+            if (j < k) pre += cj;
+            tot += cj;
+            sum += *cl.map_shared_rank(&cta_sum, j);
+        }
+        cta_prefix = pre;
+        if (k == 0) {
+            if (a.ncl) a.ncl[frame] = (int32_t)tot;
+            if (a.sizes) a.sizes[(size_t)frame * a.sizes_stride] = (int64_t)H * W - (int64_t)sum;
+        }
+    }
+    __syncthreads();
+    {
+        const uint32_t prefix = cta_prefix;
+        const uint32_t *WK = LR;
+        for (uint32_t id = tid; id < n_runs; id += kFastThreads) {
+            if (E[id] != (band | id)) continue;
+            const uint32_t km = KB[id >> 5];
+            const uint32_t b = id & 31;
+            if ((km >> b) & 1u) {
+                const uint32_t label = prefix + WK[id >> 5] + __popc(km & ((1u << b) - 1u)) + 1u;
+                if (a.sizes) a.sizes[(size_t)frame * a.sizes_stride + label] = (int64_t)SZ[id];
+                SZ[id] = label;
+            } else {
+                SZ[id] = 0;   // dropped by filter_small
+            }
+        }
+    }
+    RS_MARK(8);
+    cl.sync();   // #5: root labels are published
+
+    // ---- L. run labels, then cell labels -----------------------------------
+    for (uint32_t id = tid; id < n_runs; id += kFastThreads) {
+        const uint32_t g = E[id];
+        if (g != (band | id)) SZ[id] = *reinterpret_cast<volatile uint32_t *>(uf.slot(SZ, g));
+    }
+    RS_MARK(9);
+    cl.sync();   // #6: no DSMEM access after this point
+
+    int32_t *out = a.labels + (size_t)frame * H * W + (size_t)r0 * W;
+    if ((W & 3) == 0) {
+        // lane handles 4 consecutive cells of a word: 16-byte streaming stores
+        for (int g4 = warp; g4 * 4 < nw; g4 += kFastWarps) {
+            const int w = g4 * 4 + (lane >> 3);
+            if (w >= nw) continue;
+            const int q = divWPR(a, w);
+            const int cw = w - q * WPR;
+            const int b0 = (lane & 7) * 4;
+            const int c = cw * 32 + b0;
+            if (c >= W) continue;
+            const uint32_t pw = P[w] >> b0, sbw = SB[w], nbw = NB[w];
+            int4 lab;
+            int *lp = &lab.x;
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                lp[j] = ((pw >> j) & 1u) ? (int)SZ[nbw + __popc(sbw & lanemask_le(b0 + j)) - 1u] : 0;
+            __stcs(reinterpret_cast<int4 *>(out + q * W + c), lab);
+        }
+    } else {
+        for (int w = warp; w < nw; w += kFastWarps) {
+            const int q = divWPR(a, w);
+            const int c = (w - q * WPR) * 32 + lane;
+            if (c < W) {
+                const int lab = ((P[w] >> lane) & 1u) ? (int)SZ[run_of(SB, NB, w, lane)] : 0;
+                __stcs(out + q * W + c, lab);
+            }
+        }
+    }
+    RS_MARK(10);
+}
+
+}  // namespace rs

@@ -123,12 +123,14 @@ class Pipeline:
     """
 
     def __init__(self, model: SensorModel, config: PipelineConfig | None = None,
-                 device=None, rows_per_cta: int = 0):
+                 device=None, rows_per_cta: int = 0, node_capacity: int = 0):
         self.model = model
         self.config = config or PipelineConfig()
         self.packed = pack_tables(model, self.config)
-        self.rs_config = _native.make_config(self.packed, rows_per_cta)
+        self.rs_config = _native.make_config(self.packed, rows_per_cta, node_capacity)
         self.rows_per_cta, self.ctas_per_frame, self.smem_bytes = _native.plan(self.rs_config)
+        self.plan = _native.plan_detail(self.rs_config)
+        self._workspaces = {}
         self.device = torch.device(device if device is not None else "cuda")
         if self.device.type == "cuda" and self.device.index is None and torch.cuda.is_available():
             self.device = torch.device("cuda", torch.cuda.current_device())
@@ -154,6 +156,16 @@ class Pipeline:
         if self._tables is None:
             self._tables = torch.from_numpy(self._tables_host).to(self.device)
         return self._tables
+
+    def workspace(self, batch: int, stream) -> torch.Tensor:
+        """Zero-initialised device workspace, one per stream (the overflow list)."""
+        need = int(_native.lib().rs_workspace_size(ctypes.byref(self.rs_config), batch))
+        key = stream.cuda_stream
+        ws = self._workspaces.get(key)
+        if ws is None or ws.numel() < need:
+            ws = torch.zeros(max(need, 8), dtype=torch.uint8, device=self.device)
+            self._workspaces[key] = ws
+        return ws
 
     def _check_frames(self, ranges: torch.Tensor):
         H, W = self.shape
@@ -187,10 +199,11 @@ class Pipeline:
             cluster_sizes = None
         stride = cluster_sizes.shape[1] if cluster_sizes is not None else 0
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        ws = self.workspace(B, s)
         st = _native.lib().rs_segment_batch(
             ctypes.byref(self.rs_config), _ptr(self.device_tables()), _ptr(ranges), B,
             _ptr(labels), _ptr(n_clusters), _ptr(cluster_sizes), stride,
-            ctypes.c_void_p(s.cuda_stream))
+            _ptr(ws), ws.numel(), ctypes.c_void_p(s.cuda_stream))
         _native.check(st, "rs_segment_batch")
         return BatchResult(labels, n_clusters, cluster_sizes)
 

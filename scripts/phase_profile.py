@@ -22,8 +22,8 @@ p.add_argument("--core", action="store_true")
 p.add_argument("--skip", type=int, default=0)
 p.add_argument("--rows", type=int, default=0)
 a = p.parse_args()
-names = ["stage", "bitsA", "bitsB/MC", "runs", "local-union", "flatten+cs1", "cross+cs2",
-         "resolve+cs3", "sizes+cs4", "kept+scan+cs5", "assign+cs6", "nodelabel+cs7", "labels"]
+names = ["A bits", "B fixup/MC", "R runs", "U local+sizes", "cs1+X cross", "cs2+Z resolve",
+         "cs3+K kept", "cs4+assign", "cs5+L runlabels", "cs6+cell labels"]
 spec = synthetic.CONFIGS[a.config]
 frames = synthetic.make_batch(a.config, a.batch, device="cuda")
 cfg = (rs.PipelineConfig(mc_pattern=rs.skip_pattern(a.skip), ground_removal=False, min_cluster_points=1)
@@ -37,8 +37,9 @@ ev[0].record(); pipe.segment_batch(frames); ev[1].record(); torch.cuda.synchroni
 n = min(8192, a.batch * pipe.ctas_per_frame)
 buf = np.zeros((n, 16), dtype=np.int64)
 _native.check(_native.lib().rs_phase_profile(buf.ctypes.data_as(ctypes.c_void_p), n))
-d = np.diff(buf[:, :14], axis=1).astype(np.float64)
-tot = buf[:, 13] - buf[:, 0]
+NM = len(names) + 1
+d = np.diff(buf[:, :NM], axis=1).astype(np.float64)
+tot = buf[:, NM - 1] - buf[:, 0]
 print(f"kernel {ev[0].elapsed_time(ev[1])*1e3:.1f} us, plan R={pipe.rows_per_cta} C={pipe.ctas_per_frame} "
       f"smem={pipe.smem_bytes}, CTAs profiled {n}")
 print(f"CTA lifetime cycles: mean {tot.mean():.0f} p50 {np.median(tot):.0f} p90 {np.percentile(tot,90):.0f}")

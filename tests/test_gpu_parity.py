@@ -240,7 +240,9 @@ def test_host_buffer_entry_matches_device(config_frames):
     torch.cuda.synchronize()
     assert np.array_equal(lab, dev.labels.cpu().numpy())
     assert np.array_equal(ncl, dev.n_clusters.cpu().numpy())
-    assert np.array_equal(sz, dev.cluster_sizes.cpu().numpy())
+    dsz = dev.cluster_sizes.cpu().numpy()
+    for b in range(f.shape[0]):
+        assert np.array_equal(sz[b, :ncl[b] + 1], dsz[b, :ncl[b] + 1])
 
 
 def test_batch_zero_and_errors(cuda):
@@ -252,3 +254,29 @@ def test_batch_zero_and_errors(cuda):
         pipe.segment_batch(torch.zeros((1, 32, 1000), device="cuda:0"))
     with pytest.raises(ValueError):
         pipe.segment_batch(torch.zeros((1, 32, 1024), device="cuda:0", dtype=torch.float64))
+
+
+# ------------------------------------------------- overflow -> dense kernel ---
+@pytest.mark.parametrize("cap", [32, 700, 2000])
+@pytest.mark.parametrize("cid,variant", [(1, "default"), (4, "core"), (3, "S1")])
+def test_node_capacity_overflow_goes_to_dense_kernel(cap, cid, variant, config_frames):
+    """Frames whose bands hold more runs than the node capacity are handed to
+    the dense kernel through the overflow list; results must not change."""
+    model = synthetic.sensor_for(synthetic.CONFIGS[cid])
+    cfg = VARIANTS[variant]
+    frames = config_frames[cid]
+    pipe = rs.Pipeline(model, cfg, device="cuda:0", node_capacity=cap)
+    assert pipe.plan["fast"] and pipe.plan["may_overflow"]
+    want_l, want_n, want_s = oracle.segment_batch(frames.cpu().numpy(), pipe.packed,
+                                                  sizes_stride=pipe.sizes_stride)
+    for _ in range(2):    # the overflow list must be reset between calls
+        res = pipe.segment_batch(frames)
+        torch.cuda.synchronize()
+        assert np.array_equal(res.n_clusters.cpu().numpy(), want_n)
+        assert int((res.labels.cpu().numpy() != want_l).sum()) == 0
+        got_s = res.cluster_sizes.cpu().numpy()
+        for b in range(frames.shape[0]):
+            k = int(want_n[b])
+            assert np.array_equal(got_s[b, :k + 1], want_s[b, :k + 1])
+    ws = pipe.workspace(frames.shape[0], torch.cuda.current_stream())
+    assert int(ws[:8].view(torch.int32)[:2].abs().sum()) == 0
