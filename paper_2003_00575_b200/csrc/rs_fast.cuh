@@ -93,6 +93,29 @@ struct RunUF {
             e = gp;
         }
     }
+    // band-local find whose path-halving stores are atomicMin
+    __device__ uint32_t find_local_min(uint32_t e) const {
+        volatile uint32_t *V = E;
+        while (true) {
+            const uint32_t p = V[e & mask];
+            if (p == e) return e;
+            const uint32_t gp = V[p & mask];
+            if (gp == p) return p;
+            atomicMin(E + (e & mask), gp);
+            e = gp;
+        }
+    }
+    // cluster-wide find whose path-halving stores are atomicMin (DSMEM)
+    __device__ uint32_t find_min(uint32_t e) const {
+        while (true) {
+            const uint32_t p = ld(e);
+            if (p == e) return e;
+            const uint32_t gp = ld(p);
+            if (gp == p) return p;
+            atomicMin(slot(E, e), gp);
+            e = gp;
+        }
+    }
     __device__ void unite_local(uint32_t x, uint32_t y) const {
         while (true) {
             x = find_local(x);
@@ -388,16 +411,15 @@ __global__ void __launch_bounds__(kFastThreads, 4) rs_fast_kernel(const __grid_c
             }
         }
         __syncthreads();
+        RS_MARK(4);
         // local flatten; LR marks the band-local roots
         for (uint32_t base = warp * 32; base < n_runs; base += kFastThreads) {
             const uint32_t id = base + lane;
             bool lr = false;
             if (id < n_runs) {
-                // read-only chase: a concurrent path-halving store could
-                // otherwise replace a finished root pointer by an ancestor
-                const volatile uint32_t *V = E;
-                uint32_t r = band | id;
-                for (uint32_t p = V[r & maskN]; p != r; p = V[r & maskN]) r = p;
+                // path halving with atomicMin: entries only ever decrease, so a
+                // finished root pointer (the tree minimum) is never overwritten
+                const uint32_t r = uf.find_local_min(band | id);
                 E[id] = r;
                 lr = r == (band | id);
             }
@@ -405,6 +427,7 @@ __global__ void __launch_bounds__(kFastThreads, 4) rs_fast_kernel(const __grid_c
             if (lane == 0) LR[base >> 5] = m;
         }
         __syncthreads();
+        RS_MARK(5);
         // local component sizes: each run adds its length to its local root
         int carry = INT_MAX;   // first run end after the current chunk
         const int nchunks = (wr1 - wr0 + 31) / 32;
@@ -441,7 +464,7 @@ __global__ void __launch_bounds__(kFastThreads, 4) rs_fast_kernel(const __grid_c
             carry = __shfl_sync(kFull, inc, 0);
         }
     }
-    RS_MARK(4);
+    RS_MARK(6);
     cl.sync();   // #1: every band's runs are numbered, joined locally and sized
 
     if (tid == 0) {
@@ -456,6 +479,7 @@ __global__ void __launch_bounds__(kFastThreads, 4) rs_fast_kernel(const __grid_c
         return;
     }
 
+    RS_MARK(7);
     // ---- X. cross-band unions (DSMEM), one thread per boundary column --------
     if (r0 > 0) {
         const int ku = k - 1;
@@ -492,13 +516,14 @@ __global__ void __launch_bounds__(kFastThreads, 4) rs_fast_kernel(const __grid_c
             }
         }
     }
-    RS_MARK(5);
+    RS_MARK(8);
     cl.sync();   // #2: the forest is final
+    RS_MARK(9);
 
     // ---- Z. resolve: local roots chase their global root and add their size ---
     for (uint32_t id = tid; id < n_runs; id += kFastThreads) {
         if (!((LR[id >> 5] >> (id & 31)) & 1u)) continue;
-        const uint32_t g = uf.find_nc(band | id);
+        const uint32_t g = uf.find_min(band | id);
         if (g != (band | id)) {
             E[id] = g;
             atomicAdd(uf.slot(SZ, g), SZ[id]);
@@ -510,7 +535,7 @@ __global__ void __launch_bounds__(kFastThreads, 4) rs_fast_kernel(const __grid_c
         const uint32_t p = E[id];
         E[id] = ((p >> a.SHN) == (uint32_t)k) ? E[p & maskN] : uf.find_nc(p);
     }
-    RS_MARK(6);
+    RS_MARK(10);
     cl.sync();   // #3: sizes are final at every root
 
     // ---- K. kept roots, ordered rank ------------------------------------------
@@ -561,7 +586,7 @@ __global__ void __launch_bounds__(kFastThreads, 4) rs_fast_kernel(const __grid_c
         for (uint32_t w = tid; w < nkw; w += kFastThreads)
             WK[w] += warp_tot[min(w / max(wper, 1u), (uint32_t)kFastWarps - 1)];
     }
-    RS_MARK(7);
+    RS_MARK(11);
     cl.sync();   // #4: every band's kept count and kept-size sum are published
     if (tid == 0) {
         uint32_t pre = 0, tot = 0, sum = 0;
@@ -594,7 +619,7 @@ __global__ void __launch_bounds__(kFastThreads, 4) rs_fast_kernel(const __grid_c
             }
         }
     }
-    RS_MARK(8);
+    RS_MARK(12);
     cl.sync();   // #5: root labels are published
 
     // ---- L. run labels, then cell labels -----------------------------------
@@ -602,9 +627,10 @@ __global__ void __launch_bounds__(kFastThreads, 4) rs_fast_kernel(const __grid_c
         const uint32_t g = E[id];
         if (g != (band | id)) SZ[id] = *reinterpret_cast<volatile uint32_t *>(uf.slot(SZ, g));
     }
-    RS_MARK(9);
+    RS_MARK(13);
     cl.sync();   // #6: no DSMEM access after this point
 
+    RS_MARK(14);
     int32_t *out = a.labels + (size_t)frame * H * W + (size_t)r0 * W;
     if ((W & 3) == 0) {
         // lane handles 4 consecutive cells of a word: 16-byte streaming stores
@@ -634,7 +660,7 @@ __global__ void __launch_bounds__(kFastThreads, 4) rs_fast_kernel(const __grid_c
             }
         }
     }
-    RS_MARK(10);
+    RS_MARK(15);
 }
 
 }  // namespace rs
