@@ -107,15 +107,14 @@ __device__ __forceinline__ bool ground_rule(const KArgs &a, const GroundRow &g, 
 // as min(L,U) <= num <= max(L,U): lo <= hi and rounding is monotone, so
 // [L, U] is ordered for den > 0 and reversed for den < 0 — exactly the
 // reference's two branches; den == 0 fails either way.
-__device__ __forceinline__ bool ground_rule_mm(const KArgs &a, float sa, float ca, float lo, float hi,
+__device__ __forceinline__ bool ground_rule_mm(float mount, float keep, float sa, float ca, float lo, float hi,
                                                float sc, float d1, float d2, float v) {
     const float num = __fmul_rn(d2, sa);
     const float den = __fsub_rn(d1, __fmul_rn(d2, ca));
     const float L = __fmul_rn(lo, den);
     const float U = __fmul_rn(hi, den);
-    const bool ok = fminf(L, U) <= num && num <= fmaxf(L, U) && den != 0.f && fminf(d1, d2) > 0.f;
-    const float z = __fadd_rn(__fmul_rn(v, sc), a.mount);
-    return ok && z <= a.keep_above;
+    const float z = __fadd_rn(__fmul_rn(v, sc), mount);
+    return (fminf(L, U) <= num) & (num <= fmaxf(L, U)) & (den != 0.f) & (fminf(d1, d2) > 0.f) & (z <= keep);
 }
 
 // Presence = valid && !ground for cell (r, c); `get(row, col)` returns the range.

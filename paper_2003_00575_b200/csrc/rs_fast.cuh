@@ -132,7 +132,7 @@ struct RunUF {
 __global__ void __launch_bounds__(kFastThreads, 4) rs_fast_kernel(const __grid_constant__ KArgs a) {
     extern __shared__ __align__(128) uint32_t sm[];
     __shared__ uint32_t warp_tot[kFastWarps];
-    __shared__ uint32_t cta_cnt, cta_sum, cta_prefix, seam, ovf, ovf_any;
+    __shared__ uint32_t cta_cnt, cta_sum, cta_prefix, seam, ovf, ovf_any, n_edges, n_xedges;
     __shared__ __align__(16) float rowc[(32 + 1) * 8];   // per-row constants of the band
 
     cg::cluster_group cl = cg::this_cluster();
@@ -157,7 +157,7 @@ __global__ void __launch_bounds__(kFastThreads, 4) rs_fast_kernel(const __grid_c
     auto G = [&](int r, int c) -> float { return __ldg(fr + (size_t)r * W + c); };
 
     RS_MARK(0);
-    if (tid == 0) { seam = 0; cta_sum = 0; }
+    if (tid == 0) { seam = 0; cta_sum = 0; n_edges = 0; n_xedges = 0; }
 
     // ---- A. presence, left and up bits --------------------------------------
     // Row constants of the band (ground pair, height sine, vertical 2cos)
@@ -175,78 +175,75 @@ __global__ void __launch_bounds__(kFastThreads, 4) rs_fast_kernel(const __grid_c
     }
     __syncthreads();
     {
-        const bool vec = (W & 3) == 0;
+        // Lane l of a warp owns cells ch*128 + 32*j + l (j = 0..3) of a
+        // 128-column chunk, so a ballot of a per-cell predicate is directly
+        // the bit-plane word ch*4 + j, and the left / up edge words are
+        // warp-uniform bit operations on those words.
+        const bool ground_on = a.ground != 0;
+        const float mount = a.mount, keep = a.keep_above;
         const int nchunk = (W + 127) / 128;
         for (int ch = warp; ch < nchunk; ch += kFastWarps) {
-            const int c0 = ch * 128 + lane * 4;
-            auto ld4 = [&](int r) -> float4 {
-                const float *rowp = fr + (size_t)r * W;
-                if (vec && c0 + 3 < W) return __ldg(reinterpret_cast<const float4 *>(rowp + c0));
-                float4 x;
-                x.x = c0 < W ? __ldg(rowp + c0) : 0.f;
-                x.y = c0 + 1 < W ? __ldg(rowp + c0 + 1) : 0.f;
-                x.z = c0 + 2 < W ? __ldg(rowp + c0 + 2) : 0.f;
-                x.w = c0 + 3 < W ? __ldg(rowp + c0 + 3) : 0.f;
-                return x;
+            const int cb = ch * 128 + lane;
+            auto ld4 = [&](int r, float (&x)[4]) {
+                const float *rowp = fr + (size_t)r * W + cb;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) x[j] = cb + 32 * j < W ? __ldg(rowp + 32 * j) : 0.f;
             };
-            float4 vprev = rstart >= 1 ? ld4(rstart - 1) : make_float4(0.f, 0.f, 0.f, 0.f);
-            float4 v = ld4(rstart);
-            float4 vnext = ld4(rstart + 1);   // H >= 2; row 0 needs row 1 for its ground pair
-            uint32_t pprev = 0;
+            float va[4] = {0.f, 0.f, 0.f, 0.f}, v[4], vb[4], vn[4];
+            if (rstart >= 1) ld4(rstart - 1, va);
+            ld4(rstart, v);
+            ld4(rstart + 1, vb);   // H >= 2; row 0 needs row 1 for its ground pair
+            uint32_t pprev[4] = {0u, 0u, 0u, 0u};
             for (int r = rstart; r < rend; ++r) {
-                const float4 vn2 = (r + 2 < rend) ? ld4(r + 2) : make_float4(0.f, 0.f, 0.f, 0.f);
+                if (r + 2 < rend) ld4(r + 2, vn);
+                else {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) vn[j] = 0.f;
+                }
                 const float4 c = *reinterpret_cast<const float4 *>(rowc + (r - rstart) * 8);
                 const float2 c2 = *reinterpret_cast<const float2 *>(rowc + (r - rstart) * 8 + 4);
-                const float vv[4] = {v.x, v.y, v.z, v.w};
-                const float va[4] = {vprev.x, vprev.y, vprev.z, vprev.w};
-                const float vb[4] = {vnext.x, vnext.y, vnext.z, vnext.w};
-                uint32_t np = 0;
+                uint32_t pw[4], lw[4], uw[4];
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
-                    const float d1 = r >= 1 ? va[j] : vv[j];
-                    const float d2 = r >= 1 ? vv[j] : vb[j];
-                    bool p = vv[j] > 0.f;
-                    if (a.ground) p = p && !ground_rule_mm(a, c.x, c.y, c.z, c.w, c2.x, d1, d2, vv[j]);
-                    np |= (uint32_t)p << j;
+                    const float d1 = r >= 1 ? va[j] : v[j];
+                    const float d2 = r >= 1 ? v[j] : vb[j];
+                    const bool gr = ground_on & ground_rule_mm(mount, keep, c.x, c.y, c.z, c.w, c2.x, d1, d2, v[j]);
+                    pw[j] = __ballot_sync(kFull, (v[j] > 0.f) & !gr);
+                    // left neighbour: lane-1's cell; lane 0 takes lane 31 of word j-1
+                    // (word j = 0 starts the chunk: its bit 0 is completed in step B)
+                    const float up1 = __shfl_up_sync(kFull, v[j], 1);
+                    const float w31 = __shfl_sync(kFull, j > 0 ? v[j > 0 ? j - 1 : 0] : 0.f, 31);
+                    const float vl = lane > 0 ? up1 : w31;
+                    const uint32_t eh = __ballot_sync(kFull, pair_pass(vl, v[j], tch, thr));
+                    const uint32_t ev = __ballot_sync(kFull, pair_pass(va[j], v[j], c2.y, thr));
+                    const uint32_t pl = (pw[j] << 1) | (j > 0 ? pw[j > 0 ? j - 1 : 0] >> 31 : 0u);
+                    lw[j] = eh & pw[j] & pl;
+                    uw[j] = r > rstart ? (ev & pw[j] & pprev[j]) : 0u;
                 }
-                // left neighbour of cell j is cell j-1; cell 0 takes lane-1's cell 3
-                const float vl = __shfl_up_sync(kFull, v.w, 1);
-                const uint32_t npl = __shfl_up_sync(kFull, np, 1);
-                uint32_t nl = 0, nu = 0;
-                if (lane > 0 && (np & 1u) && (npl & 8u) && pair_pass(vl, vv[0], tch, thr)) nl |= 1u;
-#pragma unroll
-                for (int j = 1; j < 4; ++j)
-                    if (((np >> j) & 1u) && ((np >> (j - 1)) & 1u) && pair_pass(vv[j - 1], vv[j], tch, thr))
-                        nl |= 1u << j;
-                if (r > rstart) {
-#pragma unroll
-                    for (int j = 0; j < 4; ++j)
-                        if (((np & pprev) >> j) & 1u && pair_pass(va[j], vv[j], c2.y, thr)) nu |= 1u << j;
-                }
-                const int sh = (lane & 7) * 4;
-                uint32_t xp = np << sh, xl = nl << sh, xu = nu << sh;
-#pragma unroll
-                for (int m = 1; m < 8; m <<= 1) {
-                    xp |= __shfl_xor_sync(kFull, xp, m);
-                    xl |= __shfl_xor_sync(kFull, xl, m);
-                    xu |= __shfl_xor_sync(kFull, xu, m);
-                }
-                const int cw = ch * 4 + (lane >> 3);
-                if ((lane & 7) == 0 && cw < WPR) {
-                    if (r < r0) {
-                        Ph[cw] = xp;
-                        Lh[cw] = xl;
-                    } else {
-                        const int w = (r - r0) * WPR + cw;
-                        P[w] = xp;
-                        L[w] = xl;
-                        U[w] = xu;
+                if (lane < 4) {
+                    const int cw = ch * 4 + lane;
+                    const uint32_t xp = lane == 0 ? pw[0] : lane == 1 ? pw[1] : lane == 2 ? pw[2] : pw[3];
+                    const uint32_t xl = lane == 0 ? lw[0] : lane == 1 ? lw[1] : lane == 2 ? lw[2] : lw[3];
+                    const uint32_t xu = lane == 0 ? uw[0] : lane == 1 ? uw[1] : lane == 2 ? uw[2] : uw[3];
+                    if (cw < WPR) {
+                        if (r < r0) {
+                            Ph[cw] = xp;
+                            Lh[cw] = xl;
+                        } else {
+                            const int w = (r - r0) * WPR + cw;
+                            P[w] = xp;
+                            L[w] = xl;
+                            U[w] = xu;
+                        }
                     }
                 }
-                vprev = v;
-                v = vnext;
-                vnext = vn2;
-                pprev = np;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    va[j] = v[j];
+                    v[j] = vb[j];
+                    vb[j] = vn[j];
+                    pprev[j] = pw[j];
+                }
             }
         }
     }
@@ -377,37 +374,64 @@ __global__ void __launch_bounds__(kFastThreads, 4) rs_fast_kernel(const __grid_c
     const uint32_t seamw = seam;
     if (!overflow) {
         // ---- U. band-local unions ----------------------------------------------
+        // Edges are gathered into a list first so that all lanes unite in
+        // parallel (word-wise loops left ~6 of 32 lanes busy).  The size array
+        // is the buffer (zeroed again by the flatten below); an edge that does
+        // not fit is united on the spot — the union order never matters.
+        uint32_t *EL = SZ;
+        const uint32_t cap = (uint32_t)a.NC;
         for (int w = tid; w < nw; w += kFastThreads) {
             const int q = divWPR(a, w);
             const int cw = w - q * WPR;
-            const uint32_t lw = L[w], sb = SB[w];
-            if (sb & lw & 1u)   // pseudo start: join the run it continues
-                uf.unite_local(band | run_of(SB, NB, w, 0), band | run_of(SB, NB, w - 1, 31));
-            const uint32_t uw = U[w];
+            const uint32_t lw = L[w], sb = SB[w], uw = U[w];
+            const bool pseudo = (sb & lw & 1u) != 0;
+            uint32_t nru = 0;
             if (q > 0 && uw) {
                 const uint32_t uprev = (uw << 1) | (cw > 0 ? U[w - 1] >> 31 : 0u);
-                for (uint32_t nr = uw & ~(uprev & lw & L[w - WPR]); nr; nr &= nr - 1) {
-                    const int b = __ffs(nr) - 1;
-                    uf.unite_local(band | run_of(SB, NB, w, b), band | run_of(SB, NB, w - WPR, b));
-                }
+                nru = uw & ~(uprev & lw & L[w - WPR]);
             }
-            if (cw == 0 && ((seamw >> q) & 1u))
-                uf.unite_local(band | run_of(SB, NB, w, 0),
-                               band | run_of(SB, NB, q * WPR + (W - 1) / 32, (W - 1) & 31));
+            const bool sm_ = cw == 0 && ((seamw >> q) & 1u);
+            uint32_t k = (uint32_t)pseudo + __popc(nru) + (uint32_t)sm_;
             for (int o = 0; o < a.n_off; ++o) {
-                const int dy = a.dy[o];
-                if (q < dy) continue;   // partner above the band: step X
+                if (q < a.dy[o]) continue;   // partner above the band: step X
                 const uint32_t *M = MC + o * a.nwords;
                 const uint32_t m = M[w];
-                if (!m) continue;
+                const uint32_t mprev = (m << 1) | (cw > 0 ? M[w - 1] >> 31 : 0u);
+                k += __popc(m & ~(mprev & lw & TL[o * a.nwords + w]));
+            }
+            if (!k) continue;
+            uint32_t slot = atomicAdd(&n_edges, k);
+            auto push = [&](uint32_t x, uint32_t y) {
+                if (slot < cap) EL[slot] = (x << 16) | y;
+                else uf.unite_local(band | x, band | y);
+                ++slot;
+            };
+            if (pseudo) push(run_of(SB, NB, w, 0), run_of(SB, NB, w - 1, 31));
+            for (; nru; nru &= nru - 1) {
+                const int b = __ffs(nru) - 1;
+                push(run_of(SB, NB, w, b), run_of(SB, NB, w - WPR, b));
+            }
+            if (sm_) push(run_of(SB, NB, w, 0), run_of(SB, NB, q * WPR + (W - 1) / 32, (W - 1) & 31));
+            for (int o = 0; o < a.n_off; ++o) {
+                const int dy = a.dy[o];
+                if (q < dy) continue;
+                const uint32_t *M = MC + o * a.nwords;
+                const uint32_t m = M[w];
                 const uint32_t mprev = (m << 1) | (cw > 0 ? M[w - 1] >> 31 : 0u);
                 for (uint32_t nr = m & ~(mprev & lw & TL[o * a.nwords + w]); nr; nr &= nr - 1) {
                     const int b = __ffs(nr) - 1;
                     int tc = (cw * 32 + b - a.dx[o]) % W;
                     if (tc < 0) tc += W;
-                    uf.unite_local(band | run_of(SB, NB, w, b),
-                                   band | run_of(SB, NB, (q - dy) * WPR + tc / 32, tc & 31));
+                    push(run_of(SB, NB, w, b), run_of(SB, NB, (q - dy) * WPR + tc / 32, tc & 31));
                 }
+            }
+        }
+        __syncthreads();
+        {
+            const uint32_t ne = min(n_edges, cap);
+            for (uint32_t e = tid; e < ne; e += kFastThreads) {
+                const uint32_t x = EL[e];
+                uf.unite_local(band | (x >> 16), band | (x & 0xffffu));
             }
         }
         __syncthreads();
@@ -421,6 +445,7 @@ __global__ void __launch_bounds__(kFastThreads, 4) rs_fast_kernel(const __grid_c
                 // finished root pointer (the tree minimum) is never overwritten
                 const uint32_t r = uf.find_local_min(band | id);
                 E[id] = r;
+                SZ[id] = 0;   // it served as the edge list
                 lr = r == (band | id);
             }
             const uint32_t m = __ballot_sync(kFull, lr);
@@ -480,19 +505,32 @@ __global__ void __launch_bounds__(kFastThreads, 4) rs_fast_kernel(const __grid_c
     }
 
     RS_MARK(7);
-    // ---- X. cross-band unions (DSMEM), one thread per boundary column --------
+    // ---- X. cross-band unions over DSMEM -----------------------------------
+    // Boundary edges are listed first (rows 1.. of the U plane are free now and
+    // serve as the buffer), then united by all threads in parallel.
     if (r0 > 0) {
         const int ku = k - 1;
         const uint32_t *SBu = cl.map_shared_rank(SB, ku), *NBu = cl.map_shared_rank(NB, ku);
         const uint32_t bandu = (uint32_t)ku << a.SHN;
         const int wu0 = (R - 1) * WPR;
+        uint32_t *XL = U + WPR;
+        const uint32_t xcap = (uint32_t)((rows - 1) * WPR / 2);
+        auto xpush = [&](uint32_t x, uint32_t y) {
+            const uint32_t slot = atomicAdd(&n_xedges, 1u);
+            if (slot < xcap) {
+                XL[2 * slot] = x;
+                XL[2 * slot + 1] = y;
+            } else {
+                uf.unite(x, y);
+            }
+        };
         for (int c = tid; c < W; c += kFastThreads) {
             const int cw = c >> 5, b = c & 31;
             const uint32_t uw = U[cw];
             if (!((uw >> b) & 1u)) continue;
             const uint32_t upb = b > 0 ? (uw >> (b - 1)) & 1u : (cw > 0 ? U[cw - 1] >> 31 : 0u);
             if (upb && ((L[cw] >> b) & 1u) && ((Lh[cw] >> b) & 1u)) continue;   // redundant
-            uf.unite(band | run_of(SB, NB, cw, b), bandu | run_of(SBu, NBu, wu0 + cw, b));
+            xpush(band | run_of(SB, NB, cw, b), bandu | run_of(SBu, NBu, wu0 + cw, b));
         }
         for (int o = 0; o < a.n_off; ++o) {
             const int dy = a.dy[o];
@@ -510,11 +548,14 @@ __global__ void __launch_bounds__(kFastThreads, 4) rs_fast_kernel(const __grid_c
                     if (mpb && ((L[w] >> b) & 1u) && ((T[w] >> b) & 1u)) continue;
                     int tc = (c - a.dx[o]) % W;
                     if (tc < 0) tc += W;
-                    uf.unite(band | run_of(SB, NB, w, b),
-                             ((uint32_t)kt << a.SHN) | run_of(SBt, NBt, tq * WPR + tc / 32, tc & 31));
+                    xpush(band | run_of(SB, NB, w, b),
+                          ((uint32_t)kt << a.SHN) | run_of(SBt, NBt, tq * WPR + tc / 32, tc & 31));
                 }
             }
         }
+        __syncthreads();
+        const uint32_t nx = min(n_xedges, xcap);
+        for (uint32_t e = tid; e < nx; e += kFastThreads) uf.unite(XL[2 * e], XL[2 * e + 1]);
     }
     RS_MARK(8);
     cl.sync();   // #2: the forest is final
