@@ -38,8 +38,9 @@ def nvcc() -> str:
 PROF_OUT = PKG / "_lib" / "librangeseg_b200_prof.so"
 
 
-def build(force: bool = False, verbose: bool = False, profile: bool = False) -> Path:
-    out = PROF_OUT if profile else OUT
+def build(force: bool = False, verbose: bool = False, profile: bool = False,
+          out: Path | None = None, defines=()) -> Path:
+    out = out or (PROF_OUT if profile else OUT)
     deps = [SRC, INCLUDE / "rangeseg_b200.h", *HEADERS]
     if not force and out.exists() and all(out.stat().st_mtime >= d.stat().st_mtime for d in deps):
         return out
@@ -48,6 +49,8 @@ def build(force: bool = False, verbose: bool = False, profile: bool = False) -> 
     cmd = [nvcc(), *NVCC_FLAGS, "-I", str(INCLUDE), "-o", str(tmp), str(SRC)]
     if profile:
         cmd.insert(1, "-DRS_PHASE_PROF")
+    for d in defines:
+        cmd.insert(1, f"-D{d}")
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     subprocess.run(cmd, check=True)

@@ -30,9 +30,9 @@ namespace {
 constexpr int kMaxCluster = 16;
 constexpr int kMaxRowsPerCta = 31;            // seam bits of one band fit a word
 constexpr size_t kSmemLimit = 227 * 1024;     // per-CTA opt-in maximum on sm_100
-// four fast CTAs per SM: 228 KB per SM, minus 1 KB reserved and the static
-// shared memory of each CTA
-constexpr size_t kFastSmemTarget = 228 * 1024 / 4 - 1024 - 1280;
+// kFastOcc fast CTAs per SM: 228 KB per SM, minus 1 KB reserved and the
+// static shared memory of each CTA
+constexpr size_t kFastSmemTarget = 228 * 1024 / rs::kFastOcc - 1024 - 1280;
 constexpr int kMinNodeCap = 512;
 
 thread_local std::string g_err;
@@ -268,19 +268,21 @@ int set_attrs(const Plan &pl) {
 
 template <class Kern>
 int launch_cluster(Kern kern, const KArgs &k, int clusters, int threads, size_t smem, cudaStream_t stream,
-                   const char *what) {
+                   const char *what, bool dependent = false) {
     cudaLaunchConfig_t lc = {};
     lc.gridDim = dim3((unsigned)(clusters * k.C), 1, 1);
     lc.blockDim = dim3((unsigned)threads, 1, 1);
     lc.dynamicSmemBytes = smem;
     lc.stream = stream;
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = (unsigned)k.C;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
     lc.attrs = at;
-    lc.numAttrs = 1;
+    lc.numAttrs = dependent ? 2 : 1;
     return cuda_check(cudaLaunchKernelEx(&lc, kern, k), what);
 }
 
@@ -313,10 +315,13 @@ int segment_launch(const Plan &pl, const float *d_tables, const float *d_ranges,
     kf.ws = ws;
     st = launch_cluster(rs::rs_fast_kernel, kf, batch, rs::kFastThreads, pl.smem_f, stream, "rs_fast_kernel launch");
     if (st || !pl.may_overflow) return st;
+    // Overflow pass: a few persistent clusters walk the (usually empty) list;
+    // a programmatic dependent launch hides its launch latency behind the
+    // fast kernel's tail.
     kd.list_mode = 1;
-    const int G = std::max(1, std::min<int>(batch, 128 / kd.C));
+    const int G = std::max(1, std::min<int>(batch, 32 / kd.C));
     return launch_cluster(rs::rs_dense_kernel, kd, G, rs::kDenseThreads, pl.smem_d, stream,
-                          "rs_dense_kernel (overflow) launch");
+                          "rs_dense_kernel (overflow) launch", true);
 }
 
 size_t workspace_bytes(int32_t batch) { return (size_t)(2 + std::max(batch, 0)) * sizeof(int); }

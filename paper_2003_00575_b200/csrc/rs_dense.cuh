@@ -597,6 +597,9 @@ __global__ void __launch_bounds__(kDenseThreads, 1) rs_dense_kernel(const __grid
         return;
     }
     cg::cluster_group cl = cg::this_cluster();
+    // launched as a programmatic dependent of rs_fast_kernel: wait until its
+    // grid has completed and its writes (the overflow list) are visible
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     const int G = gridDim.x / a.C;
     const int count = *reinterpret_cast<volatile int *>(a.ws);
     uint32_t it = 0;

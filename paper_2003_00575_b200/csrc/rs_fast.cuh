@@ -31,7 +31,11 @@
 
 namespace rs {
 
+#ifndef RS_FAST_OCC
+#define RS_FAST_OCC 4
+#endif
 constexpr int kFastThreads = 256;
+constexpr int kFastOcc = RS_FAST_OCC;   // CTAs per SM the fast kernel is sized for
 constexpr int kFastWarps = kFastThreads / 32;
 
 // Run id of cell bit b of word w: runs started at or before the cell in this
@@ -129,7 +133,7 @@ struct RunUF {
     }
 };
 
-__global__ void __launch_bounds__(kFastThreads, 4) rs_fast_kernel(const __grid_constant__ KArgs a) {
+__global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const __grid_constant__ KArgs a) {
     extern __shared__ __align__(128) uint32_t sm[];
     __shared__ uint32_t warp_tot[kFastWarps];
     __shared__ uint32_t cta_cnt, cta_sum, cta_prefix, seam, ovf, ovf_any, n_edges, n_xedges;
@@ -501,6 +505,7 @@ __global__ void __launch_bounds__(kFastThreads, 4) rs_fast_kernel(const __grid_c
     if (ovf_any) {   // cluster-uniform: the dense kernel takes this frame
         if (k == 0 && tid == 0) a.ws[2 + atomicAdd(a.ws, 1)] = frame;
         cl.sync();
+        asm volatile("griddepcontrol.launch_dependents;");
         return;
     }
 
@@ -702,6 +707,8 @@ __global__ void __launch_bounds__(kFastThreads, 4) rs_fast_kernel(const __grid_c
         }
     }
     RS_MARK(15);
+    // let the overflow pass (a programmatic dependent launch) get scheduled
+    asm volatile("griddepcontrol.launch_dependents;");
 }
 
 }  // namespace rs
