@@ -28,11 +28,12 @@ using rs::KArgs;
 namespace {
 
 constexpr int kMaxCluster = 16;
-constexpr int kMaxRowsPerCta = 31;            // seam bits of one band fit a word
+constexpr int kMaxRowsPerCta = 31;            // dense kernel: seam bits of band + halo fit a word
+constexpr int kMaxRowsFast = 64;              // fast kernel: two seam words
 constexpr size_t kSmemLimit = 227 * 1024;     // per-CTA opt-in maximum on sm_100
 // kFastOcc fast CTAs per SM: 228 KB per SM, minus 1 KB reserved and the
 // static shared memory of each CTA
-constexpr size_t kFastSmemTarget = 228 * 1024 / rs::kFastOcc - 1024 - 1280;
+constexpr size_t kFastSmemTarget = 228 * 1024 / rs::kFastOcc - 1024 - 2560;
 constexpr int kMinNodeCap = 512;
 
 thread_local std::string g_err;
@@ -63,8 +64,8 @@ int validate(const rs_config *cfg) {
             return fail(RS_EINVAL, "offset (" + std::to_string(dy) + ", " + std::to_string(dx) +
                                        ") exceeds frame " + std::to_string(H) + "x" + std::to_string(W));
     }
-    if (cfg->rows_per_cta < 0 || cfg->rows_per_cta > kMaxRowsPerCta)
-        return fail(RS_EINVAL, "rows_per_cta must be in [0, 31]");
+    if (cfg->rows_per_cta < 0 || cfg->rows_per_cta > kMaxRowsFast)
+        return fail(RS_EINVAL, "rows_per_cta must be in [0, 64]");
     return RS_OK;
 }
 
@@ -172,7 +173,8 @@ int make_plan(const rs_config *cfg, Plan *pl) {
     const int H = cfg->height, W = cfg->width, n_off = cfg->n_offsets;
 
     // dense plan (fallback / overflow path)
-    const int Rd = cfg->rows_per_cta > 0 ? std::min(cfg->rows_per_cta, H) : pick_dense_rows(cfg);
+    int Rd = cfg->rows_per_cta > 0 ? std::min({cfg->rows_per_cta, H, kMaxRowsPerCta}) : pick_dense_rows(cfg);
+    if (dense_layout(Rd, W, n_off, nullptr) > kSmemLimit) Rd = pick_dense_rows(cfg);
     const int Cd = (H + Rd - 1) / Rd;
     const size_t smem_d = dense_layout(Rd, W, n_off, nullptr);
     if (Cd > kMaxCluster)
@@ -189,44 +191,44 @@ int make_plan(const rs_config *cfg, Plan *pl) {
     pl->smem_d = smem_d;
 
     // fast plan: ~16K cells per band, node capacity from the shared-memory target
-    int Rf = cfg->rows_per_cta > 0 ? std::min(cfg->rows_per_cta, H)
-                                   : std::min({H, kMaxRowsPerCta, std::max(1, 16384 / std::max(W, 1))});
-    while (cfg->rows_per_cta <= 0 && (H + Rf - 1) / Rf > kMaxCluster && Rf < kMaxRowsPerCta) ++Rf;
+    // ~64K cells per band: fewer, larger bands mean fewer cross-band edges and
+    // cheaper cluster barriers (measured: 2 bands of 32 rows beat 8 of 8 for
+    // 64x2048 frames).  Many Map Connection bit planes shrink the band until
+    // the run capacity is at least an eighth of its cells (observed: <= 10% for
+    // 32-row bands of the BASELINE configs; more overflows to the dense kernel).
     pl->fast = false;
     pl->may_overflow = false;
     pl->smem_f = 0;
     memset(&pl->kf, 0, sizeof(pl->kf));
-    if ((H + Rf - 1) / Rf <= kMaxCluster) {
+    int Rf = cfg->rows_per_cta > 0 ? std::min(cfg->rows_per_cta, H)
+                                   : std::min({H, kMaxRowsFast, std::max(1, 65536 / std::max(W, 1))});
+    while (cfg->rows_per_cta <= 0 && (H + Rf - 1) / Rf > kMaxCluster && Rf < kMaxRowsFast) ++Rf;
+    for (; Rf >= 1; Rf = cfg->rows_per_cta > 0 ? 0 : Rf / 2) {
+        if ((H + Rf - 1) / Rf > kMaxCluster) break;
         const int cap_full = max_runs(Rf, W);
-        long long NC = cap_full;
-        if (fast_layout(Rf, W, n_off, (int)NC, nullptr) > kFastSmemTarget) {
-            // largest capacity that keeps four CTAs per SM
-            long long lo = 0, hi = cap_full;
-            while (lo < hi) {
-                const long long mid = (lo + hi + 1) / 2;
-                if (fast_layout(Rf, W, n_off, (int)mid, nullptr) <= kFastSmemTarget) lo = mid; else hi = mid - 1;
-            }
-            NC = lo;
-            // many Map Connection bit planes: give up occupancy before capacity
-            if (NC < 2048) NC = std::min<long long>(cap_full, 4096);
+        long long lo = 0, hi = cap_full;   // largest capacity under the shared-memory target
+        while (lo < hi) {
+            const long long mid = (lo + hi + 1) / 2;
+            if (fast_layout(Rf, W, n_off, (int)mid, nullptr) <= kFastSmemTarget) lo = mid; else hi = mid - 1;
         }
+        long long NC = lo;
         if (cfg->reserved[0] > 0) NC = std::min<long long>(NC, cfg->reserved[0]);   // test hook
         if (NC < cap_full) NC &= ~31LL;
-        if (NC >= std::min(kMinNodeCap, cap_full) || cfg->reserved[0] > 0) {
-            NC = std::max<long long>(NC, 32);
-            const size_t smem_f = fast_layout(Rf, W, n_off, (int)NC, nullptr);
-            if (smem_f <= kSmemLimit) {
-                fill_common(cfg, Rf, pl->kf);
-                fast_layout(Rf, W, n_off, (int)NC, &pl->kf);
-                pl->kf.NC = (int)NC;
-                int SHN = 0;
-                while ((1 << SHN) < NC) ++SHN;
-                pl->kf.SHN = SHN;
-                pl->smem_f = smem_f;
-                pl->fast = true;
-                pl->may_overflow = NC < cap_full;
-            }
-        }
+        const long long need = std::min<long long>(cap_full, std::max<long long>(kMinNodeCap, (long long)Rf * W / 8));
+        if (NC < need && cfg->reserved[0] <= 0) continue;
+        NC = std::max<long long>(NC, 32);
+        const size_t smem_f = fast_layout(Rf, W, n_off, (int)NC, nullptr);
+        if (smem_f > kSmemLimit) continue;
+        fill_common(cfg, Rf, pl->kf);
+        fast_layout(Rf, W, n_off, (int)NC, &pl->kf);
+        pl->kf.NC = (int)NC;
+        int SHN = 0;
+        while ((1 << SHN) < NC) ++SHN;
+        pl->kf.SHN = SHN;
+        pl->smem_f = smem_f;
+        pl->fast = true;
+        pl->may_overflow = NC < cap_full;
+        break;
     }
     return RS_OK;
 }

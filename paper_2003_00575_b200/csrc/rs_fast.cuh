@@ -1,8 +1,9 @@
 // rs_fast.cuh — the fast kernel: union-find over compactly numbered runs.
 //
-// One thread-block cluster per frame, one 256-thread CTA per band of R rows
-// spanning the full width (so the azimuth seam is CTA-local).  Shared memory
-// holds only bit planes and per-run state, so four CTAs share an SM:
+// One thread-block cluster per frame, one 512-thread CTA per band of R rows
+// (about 64K cells: two bands for a 64x2048 frame) spanning the full width,
+// so the azimuth seam is CTA-local.  Shared memory holds only bit planes and
+// per-run state, so two CTAs share an SM:
 //
 //   A  presence / left / up edge bits straight from global memory: each warp
 //      walks 32-column strips down the band, keeping the row above in
@@ -32,9 +33,12 @@
 namespace rs {
 
 #ifndef RS_FAST_OCC
-#define RS_FAST_OCC 4
+#define RS_FAST_OCC 2
 #endif
-constexpr int kFastThreads = 256;
+#ifndef RS_FAST_THREADS
+#define RS_FAST_THREADS 512
+#endif
+constexpr int kFastThreads = RS_FAST_THREADS;
 constexpr int kFastOcc = RS_FAST_OCC;   // CTAs per SM the fast kernel is sized for
 constexpr int kFastWarps = kFastThreads / 32;
 
@@ -136,8 +140,9 @@ struct RunUF {
 __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const __grid_constant__ KArgs a) {
     extern __shared__ __align__(128) uint32_t sm[];
     __shared__ uint32_t warp_tot[kFastWarps];
-    __shared__ uint32_t cta_cnt, cta_sum, cta_prefix, seam, ovf, ovf_any, n_edges, n_xedges;
-    __shared__ __align__(16) float rowc[(32 + 1) * 8];   // per-row constants of the band
+    __shared__ uint32_t cta_cnt, cta_sum, cta_prefix, ovf, ovf_any, n_edges, n_xedges;
+    __shared__ uint32_t seam[2];   // seam edge per own row (R <= 64)
+    __shared__ __align__(16) float rowc[(64 + 1) * 8];   // per-row constants of the band
 
     cg::cluster_group cl = cg::this_cluster();
     const int k = (int)cl.block_rank();
@@ -161,7 +166,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
     auto G = [&](int r, int c) -> float { return __ldg(fr + (size_t)r * W + c); };
 
     RS_MARK(0);
-    if (tid == 0) { seam = 0; cta_sum = 0; n_edges = 0; n_xedges = 0; }
+    if (tid == 0) { seam[0] = seam[1] = 0; cta_sum = 0; n_edges = 0; n_xedges = 0; }
 
     // ---- A. presence, left and up bits --------------------------------------
     // Row constants of the band (ground pair, height sine, vertical 2cos)
@@ -279,7 +284,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
             const int r = r0 + q;
             const uint32_t pe = P[q * WPR + (W - 1) / 32] >> ((W - 1) & 31);
             if ((pe & 1u) && (P[q * WPR] & 1u) && pair_pass(G(r, W - 1), G(r, 0), tch, thr))
-                atomicOr(&seam, 1u << q);
+                atomicOr(&seam[q >> 5], 1u << (q & 31));
         }
     }
     if (a.n_off > 0) {
@@ -375,7 +380,6 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
     RS_MARK(3);
 
     RunUF uf{E, cl, maskN, a.SHN, k};
-    const uint32_t seamw = seam;
     if (!overflow) {
         // ---- U. band-local unions ----------------------------------------------
         // Edges are gathered into a list first so that all lanes unite in
@@ -394,7 +398,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
                 const uint32_t uprev = (uw << 1) | (cw > 0 ? U[w - 1] >> 31 : 0u);
                 nru = uw & ~(uprev & lw & L[w - WPR]);
             }
-            const bool sm_ = cw == 0 && ((seamw >> q) & 1u);
+            const bool sm_ = cw == 0 && ((seam[q >> 5] >> (q & 31)) & 1u);
             uint32_t k = (uint32_t)pseudo + __popc(nru) + (uint32_t)sm_;
             for (int o = 0; o < a.n_off; ++o) {
                 if (q < a.dy[o]) continue;   // partner above the band: step X

@@ -140,7 +140,7 @@ def test_tables_count_matches_layout():
         assert lib.rs_tables_count(H, n) == rs.PackedTables.size(H, n)
 
 
-@pytest.mark.parametrize("H,W,R,C", [(64, 2048, 8, 8), (32, 1024, 16, 2), (8, 16, 8, 1),
+@pytest.mark.parametrize("H,W,R,C", [(64, 2048, 32, 2), (32, 1024, 32, 1), (8, 16, 8, 1),
                                      (3, 5, 3, 1), (128, 2048, None, None),
                                      (64, 4000, None, None), (200, 1000, None, None)])
 def test_plan(H, W, R, C):
