@@ -124,13 +124,14 @@ size_t fast_layout(int R, int W, int n_off, int NC, KArgs *k) {
     const int ncw = (NC + 31) / 32;
     int off = 0;
     int o[12];
-    o[0] = off; off += nwords;          // P
-    o[1] = off; off += nwords;          // L
-    o[2] = off; off += nwords;          // U
-    o[3] = off; off += nwords;          // SB
-    o[4] = off; off += nwords;          // NB (run ids before each word)
-    o[5] = off; off += WPR;             // Ph
-    o[6] = off; off += WPR;             // Lh
+    const int nw4 = (nwords + 3) & ~3, wpr4 = (WPR + 3) & ~3;   // 16-byte aligned planes
+    o[0] = off; off += nw4;             // P
+    o[1] = off; off += nw4;             // L
+    o[2] = off; off += nw4;             // U
+    o[3] = off; off += nw4;             // SB
+    o[4] = off; off += nw4;             // NB (run ids before each word)
+    o[5] = off; off += wpr4;            // Ph
+    o[6] = off; off += wpr4;            // Lh
     o[7] = off; off += n_off * nwords;  // MC
     o[8] = off; off += n_off * nwords;  // TL
     o[9] = off; off += ncw;             // LR (band-local roots), later kept-word prefixes

@@ -137,6 +137,115 @@ struct RunUF {
     }
 };
 
+// Step A for one 128-column chunk: lane l owns cells ch*128 + 32*j + l
+// (j = 0..3), so a ballot of a per-cell predicate is directly the bit-plane
+// word ch*4 + j and the left / up edge words are warp-uniform bit operations.
+// The warp walks rows rfirst..rend-1 with the row above in registers and a
+// two-row prefetch; four rotating register sets (unrolled by four) avoid
+// register moves.  Row 0 (whose ground pair is rows 0/1) is done by a
+// separate ROW0 step.  FULL: the chunk lies inside the row (no load guards,
+// 16-byte stores of the four words by lane 0).
+template <bool FULL>
+struct BitsStrip {
+    const KArgs &a;
+    const float *col;
+    const float *rowc;
+    uint32_t *P, *L, *U, *Ph, *Lh;
+    int ch, lane, r0, rstart, rend, cb;
+    float thr, tch, mount, keep;
+    bool ground_on;
+
+    __device__ __forceinline__ void ld4(int r, float (&x)[4], bool pred = true) const {
+        const float *p = col + (size_t)r * a.W;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if (pred && (FULL || cb + 32 * j < a.W)) x[j] = __ldg(p + 32 * j);
+            else if (!FULL) x[j] = 0.f;
+    }
+
+    // va = row above, v = this row, vb = row below; vn <- row r+2
+    template <bool ROW0>
+    __device__ __forceinline__ void step(int r, const float (&va)[4], const float (&v)[4], const float (&vb)[4],
+                                         float (&vn)[4], const uint32_t (&pin)[4], uint32_t (&pout)[4]) const {
+        ld4(r + 2, vn, r + 2 < rend);
+        const float4 c = *reinterpret_cast<const float4 *>(rowc + (r - rstart) * 8);
+        const float2 c2 = *reinterpret_cast<const float2 *>(rowc + (r - rstart) * 8 + 4);
+        const int srcl = (lane + 31) & 31;
+        const bool last = lane == 31;
+        uint32_t lw[4], uw[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const float d1 = ROW0 ? v[j] : va[j];
+            const float d2 = ROW0 ? vb[j] : v[j];
+            const bool gr = ground_on & ground_rule_mm(mount, keep, c.x, c.y, c.z, c.w, c2.x, d1, d2, v[j]);
+            pout[j] = __ballot_sync(kFull, (v[j] > 0.f) & !gr);
+            // left neighbour: lane l-1's cell; lane 0 reads lane 31's cell of
+            // word j-1 (word 0 of the chunk: bit 0 is completed in step B)
+            const float src = (j > 0 && last) ? v[j > 0 ? j - 1 : 0] : v[j];
+            const float vl = __shfl_sync(kFull, src, srcl);
+            const uint32_t eh = __ballot_sync(kFull, pair_pass(vl, v[j], tch, thr));
+            const uint32_t ev = __ballot_sync(kFull, pair_pass(va[j], v[j], c2.y, thr));
+            const uint32_t pl = (pout[j] << 1) | (j > 0 ? pout[j > 0 ? j - 1 : 0] >> 31 : 0u);
+            lw[j] = eh & pout[j] & (j > 0 ? pl : pl & ~1u);
+            uw[j] = ROW0 ? 0u : (ev & pout[j] & pin[j]);
+        }
+        const bool halo = r < r0;
+        const int cw = ch * 4;
+        if (FULL) {
+            if (lane == 0) {
+                const int w = halo ? 0 : (r - r0) * a.WPR + cw;
+                uint32_t *dp = halo ? Ph + cw : P + w, *dl = halo ? Lh + cw : L + w;
+                *reinterpret_cast<uint4 *>(dp) = make_uint4(pout[0], pout[1], pout[2], pout[3]);
+                *reinterpret_cast<uint4 *>(dl) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+                if (!halo) *reinterpret_cast<uint4 *>(U + w) = make_uint4(uw[0], uw[1], uw[2], uw[3]);
+            }
+        } else if (lane < 4 && cw + lane < a.WPR) {
+            const uint32_t xp = lane == 0 ? pout[0] : lane == 1 ? pout[1] : lane == 2 ? pout[2] : pout[3];
+            const uint32_t xl = lane == 0 ? lw[0] : lane == 1 ? lw[1] : lane == 2 ? lw[2] : lw[3];
+            const uint32_t xu = lane == 0 ? uw[0] : lane == 1 ? uw[1] : lane == 2 ? uw[2] : uw[3];
+            if (halo) {
+                Ph[cw + lane] = xp;
+                Lh[cw + lane] = xl;
+            } else {
+                const int w = (r - r0) * a.WPR + cw + lane;
+                P[w] = xp;
+                L[w] = xl;
+                U[w] = xu;
+            }
+        }
+    }
+
+    __device__ __forceinline__ void run() const {
+        float S0[4], S1[4], S2[4], S3[4];
+        uint32_t Q0[4] = {0u, 0u, 0u, 0u}, Q1[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) S0[j] = S1[j] = S2[j] = S3[j] = 0.f;
+        int rf = rstart;
+        if (rstart == 0) {   // row 0: ground pair (0, 1), no up edges
+            ld4(0, S1);
+            ld4(1, S2);
+            step<true>(0, S0, S1, S2, S3, Q0, Q1);
+            rf = 1;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) Q0[j] = Q1[j];
+        }
+        if (rf >= rend) return;
+        if (rf >= 1) ld4(rf - 1, S0);
+        ld4(rf, S1);
+        ld4(rf + 1, S2, rf + 1 < rend);
+        // the first row walked in a band > 0 is the halo row: no up bits needed
+        for (int r = rf; r < rend; r += 4) {
+            step<false>(r, S0, S1, S2, S3, Q0, Q1);
+            if (r + 1 >= rend) break;
+            step<false>(r + 1, S1, S2, S3, S0, Q1, Q0);
+            if (r + 2 >= rend) break;
+            step<false>(r + 2, S2, S3, S0, S1, Q0, Q1);
+            if (r + 3 >= rend) break;
+            step<false>(r + 3, S3, S0, S1, S2, Q1, Q0);
+        }
+    }
+};
+
 __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const __grid_constant__ KArgs a) {
     extern __shared__ __align__(128) uint32_t sm[];
     __shared__ uint32_t warp_tot[kFastWarps];
@@ -184,76 +293,15 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
     }
     __syncthreads();
     {
-        // Lane l of a warp owns cells ch*128 + 32*j + l (j = 0..3) of a
-        // 128-column chunk, so a ballot of a per-cell predicate is directly
-        // the bit-plane word ch*4 + j, and the left / up edge words are
-        // warp-uniform bit operations on those words.
-        const bool ground_on = a.ground != 0;
-        const float mount = a.mount, keep = a.keep_above;
         const int nchunk = (W + 127) / 128;
         for (int ch = warp; ch < nchunk; ch += kFastWarps) {
             const int cb = ch * 128 + lane;
-            auto ld4 = [&](int r, float (&x)[4]) {
-                const float *rowp = fr + (size_t)r * W + cb;
-#pragma unroll
-                for (int j = 0; j < 4; ++j) x[j] = cb + 32 * j < W ? __ldg(rowp + 32 * j) : 0.f;
-            };
-            float va[4] = {0.f, 0.f, 0.f, 0.f}, v[4], vb[4], vn[4];
-            if (rstart >= 1) ld4(rstart - 1, va);
-            ld4(rstart, v);
-            ld4(rstart + 1, vb);   // H >= 2; row 0 needs row 1 for its ground pair
-            uint32_t pprev[4] = {0u, 0u, 0u, 0u};
-            for (int r = rstart; r < rend; ++r) {
-                if (r + 2 < rend) ld4(r + 2, vn);
-                else {
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) vn[j] = 0.f;
-                }
-                const float4 c = *reinterpret_cast<const float4 *>(rowc + (r - rstart) * 8);
-                const float2 c2 = *reinterpret_cast<const float2 *>(rowc + (r - rstart) * 8 + 4);
-                uint32_t pw[4], lw[4], uw[4];
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const float d1 = r >= 1 ? va[j] : v[j];
-                    const float d2 = r >= 1 ? v[j] : vb[j];
-                    const bool gr = ground_on & ground_rule_mm(mount, keep, c.x, c.y, c.z, c.w, c2.x, d1, d2, v[j]);
-                    pw[j] = __ballot_sync(kFull, (v[j] > 0.f) & !gr);
-                    // left neighbour: lane-1's cell; lane 0 takes lane 31 of word j-1
-                    // (word j = 0 starts the chunk: its bit 0 is completed in step B)
-                    const float up1 = __shfl_up_sync(kFull, v[j], 1);
-                    const float w31 = __shfl_sync(kFull, j > 0 ? v[j > 0 ? j - 1 : 0] : 0.f, 31);
-                    const float vl = lane > 0 ? up1 : w31;
-                    const uint32_t eh = __ballot_sync(kFull, pair_pass(vl, v[j], tch, thr));
-                    const uint32_t ev = __ballot_sync(kFull, pair_pass(va[j], v[j], c2.y, thr));
-                    const uint32_t pl = (pw[j] << 1) | (j > 0 ? pw[j > 0 ? j - 1 : 0] >> 31 : 0u);
-                    lw[j] = eh & pw[j] & pl;
-                    uw[j] = r > rstart ? (ev & pw[j] & pprev[j]) : 0u;
-                }
-                if (lane < 4) {
-                    const int cw = ch * 4 + lane;
-                    const uint32_t xp = lane == 0 ? pw[0] : lane == 1 ? pw[1] : lane == 2 ? pw[2] : pw[3];
-                    const uint32_t xl = lane == 0 ? lw[0] : lane == 1 ? lw[1] : lane == 2 ? lw[2] : lw[3];
-                    const uint32_t xu = lane == 0 ? uw[0] : lane == 1 ? uw[1] : lane == 2 ? uw[2] : uw[3];
-                    if (cw < WPR) {
-                        if (r < r0) {
-                            Ph[cw] = xp;
-                            Lh[cw] = xl;
-                        } else {
-                            const int w = (r - r0) * WPR + cw;
-                            P[w] = xp;
-                            L[w] = xl;
-                            U[w] = xu;
-                        }
-                    }
-                }
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    va[j] = v[j];
-                    v[j] = vb[j];
-                    vb[j] = vn[j];
-                    pprev[j] = pw[j];
-                }
-            }
+            if (ch * 128 + 128 <= W && (WPR & 3) == 0)
+                BitsStrip<true>{a, fr + cb, rowc, P, L, U, Ph, Lh, ch, lane, r0, rstart, rend, cb,
+                                thr, tch, a.mount, a.keep_above, a.ground != 0}.run();
+            else
+                BitsStrip<false>{a, fr + cb, rowc, P, L, U, Ph, Lh, ch, lane, r0, rstart, rend, cb,
+                                 thr, tch, a.mount, a.keep_above, a.ground != 0}.run();
         }
     }
     __syncthreads();
