@@ -85,7 +85,8 @@ def check(status: int, what: str = "rangeseg_b200"):
     raise RuntimeError(f"{what}: {msg}")
 
 
-def make_config(packed, rows_per_cta: int = 0, node_capacity: int = 0) -> RsConfig:
+def make_config(packed, rows_per_cta: int = 0, node_capacity: int = 0,
+                stop_after: int = 0) -> RsConfig:
     if len(packed.offsets) > MAX_OFFSETS:
         raise ValueError(f"at most {MAX_OFFSETS} Map Connection offsets are supported")
     cfg = RsConfig()
@@ -101,6 +102,7 @@ def make_config(packed, rows_per_cta: int = 0, node_capacity: int = 0) -> RsConf
     cfg.two_cos_h = float(packed.two_cos_h)
     cfg.rows_per_cta = int(rows_per_cta)
     cfg.reserved[0] = int(node_capacity)
+    cfg.reserved[1] = int(stop_after)   # experiments only: truncated kernel, wrong labels
     return cfg
 
 

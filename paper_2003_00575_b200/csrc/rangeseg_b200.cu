@@ -156,6 +156,7 @@ struct Plan {
     bool may_overflow;    // fast kernel may hand frames to the dense kernel
     KArgs kf, kd;         // arguments of the fast / dense kernels
     size_t smem_f, smem_d;
+    int stop_after;       // experiments (rs_config.reserved[1]); 0 in production
 };
 
 int pick_dense_rows(const rs_config *cfg) {
@@ -172,6 +173,7 @@ int make_plan(const rs_config *cfg, Plan *pl) {
     int st = validate(cfg);
     if (st) return st;
     const int H = cfg->height, W = cfg->width, n_off = cfg->n_offsets;
+    pl->stop_after = cfg->reserved[1];
 
     // dense plan (fallback / overflow path)
     int Rd = cfg->rows_per_cta > 0 ? std::min({cfg->rows_per_cta, H, kMaxRowsPerCta}) : pick_dense_rows(cfg);
@@ -316,6 +318,7 @@ int segment_launch(const Plan &pl, const float *d_tables, const float *d_ranges,
     kf.sizes = d_cluster_sizes;
     kf.sizes_stride = sizes_stride;
     kf.ws = ws;
+    kf.stop_after = pl.stop_after;
     st = launch_cluster(rs::rs_fast_kernel, kf, batch, rs::kFastThreads, pl.smem_f, stream, "rs_fast_kernel launch");
     if (st || !pl.may_overflow) return st;
     // Overflow pass: a few persistent clusters walk the (usually empty) list;

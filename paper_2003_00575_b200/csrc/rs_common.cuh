@@ -38,6 +38,7 @@ struct KArgs {
     int use_tma;                  // dense kernel: stage rows with TMA bulk copies
     int *ws;                      // [0] overflow count, [1] done counter, [2..] frame list
     int list_mode;                // dense kernel: process the overflow list
+    int stop_after;               // experiments only: leave the fast kernel after phase N (0 = never)
 };
 
 // ------------------------------------------------------------ phase markers

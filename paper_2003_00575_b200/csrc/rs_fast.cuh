@@ -306,6 +306,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
     }
     __syncthreads();
     RS_MARK(1);
+    if (a.stop_after == 1) { cl.sync(); return; }
 
     // ---- B. word-boundary left bits, seam, Map Connection bits ---------------
     for (int w = tid; w < nw + WPR; w += kFastThreads) {
@@ -426,6 +427,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
     }
     __syncthreads();
     RS_MARK(3);
+    if (a.stop_after == 2) { cl.sync(); return; }
 
     RunUF uf{E, cl, maskN, a.SHN, k};
     if (!overflow) {
@@ -436,27 +438,38 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
         // not fit is united on the spot — the union order never matters.
         uint32_t *EL = SZ;
         const uint32_t cap = (uint32_t)a.NC;
-        for (int w = tid; w < nw; w += kFastThreads) {
-            const int q = divWPR(a, w);
+        for (int wb = warp * 32; wb < nw; wb += kFastThreads) {
+            const int w = wb + lane;
+            const bool act = w < nw;
+            const int q = act ? divWPR(a, w) : 0;
             const int cw = w - q * WPR;
-            const uint32_t lw = L[w], sb = SB[w], uw = U[w];
+            const uint32_t lw = act ? L[w] : 0u, sb = act ? SB[w] : 0u, uw = act ? U[w] : 0u;
             const bool pseudo = (sb & lw & 1u) != 0;
             uint32_t nru = 0;
             if (q > 0 && uw) {
                 const uint32_t uprev = (uw << 1) | (cw > 0 ? U[w - 1] >> 31 : 0u);
                 nru = uw & ~(uprev & lw & L[w - WPR]);
             }
-            const bool sm_ = cw == 0 && ((seam[q >> 5] >> (q & 31)) & 1u);
+            const bool sm_ = act && cw == 0 && ((seam[q >> 5] >> (q & 31)) & 1u);
             uint32_t k = (uint32_t)pseudo + __popc(nru) + (uint32_t)sm_;
-            for (int o = 0; o < a.n_off; ++o) {
+            for (int o = 0; o < a.n_off && act; ++o) {
                 if (q < a.dy[o]) continue;   // partner above the band: step X
                 const uint32_t *M = MC + o * a.nwords;
                 const uint32_t m = M[w];
                 const uint32_t mprev = (m << 1) | (cw > 0 ? M[w - 1] >> 31 : 0u);
                 k += __popc(m & ~(mprev & lw & TL[o * a.nwords + w]));
             }
+            // warp-aggregated reservation in the edge list
+            uint32_t inc = k;
+            for (int off = 1; off < 32; off <<= 1) {
+                const uint32_t t = __shfl_up_sync(kFull, inc, off);
+                if (lane >= off) inc += t;
+            }
+            uint32_t wbase = 0;
+            if (lane == 31 && inc) wbase = atomicAdd(&n_edges, inc);
+            wbase = __shfl_sync(kFull, wbase, 31);
             if (!k) continue;
-            uint32_t slot = atomicAdd(&n_edges, k);
+            uint32_t slot = wbase + inc - k;
             auto push = [&](uint32_t x, uint32_t y) {
                 if (slot < cap) EL[slot] = (x << 16) | y;
                 else uf.unite_local(band | x, band | y);
@@ -483,15 +496,22 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
             }
         }
         __syncthreads();
+        if (a.stop_after == 9) { cl.sync(); return; }
         {
+            // contiguous slices per thread: edges next to each other in the list
+            // mostly join the same components, so neighbouring threads taking
+            // neighbouring edges would contend on the same roots
             const uint32_t ne = min(n_edges, cap);
-            for (uint32_t e = tid; e < ne; e += kFastThreads) {
+            const uint32_t per = (ne + kFastThreads - 1) / kFastThreads;
+            const uint32_t e0 = min(tid * per, ne), e1 = min(e0 + per, ne);
+            for (uint32_t e = e0; e < e1; ++e) {
                 const uint32_t x = EL[e];
                 uf.unite_local(band | (x >> 16), band | (x & 0xffffu));
             }
         }
         __syncthreads();
         RS_MARK(4);
+    if (a.stop_after == 3) { cl.sync(); return; }
         // local flatten; LR marks the band-local roots
         for (uint32_t base = warp * 32; base < n_runs; base += kFastThreads) {
             const uint32_t id = base + lane;
@@ -545,6 +565,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
             carry = __shfl_sync(kFull, inc, 0);
         }
     }
+    if (a.stop_after == 4) { cl.sync(); return; }
     RS_MARK(6);
     cl.sync();   // #1: every band's runs are numbered, joined locally and sized
 
@@ -572,8 +593,15 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
         const int wu0 = (R - 1) * WPR;
         uint32_t *XL = U + WPR;
         const uint32_t xcap = (uint32_t)((rows - 1) * WPR / 2);
-        auto xpush = [&](uint32_t x, uint32_t y) {
-            const uint32_t slot = atomicAdd(&n_xedges, 1u);
+        // warp-aggregated: every lane calls, `has` lanes push an edge
+        auto xpush = [&](bool has, uint32_t x, uint32_t y) {
+            const uint32_t m = __ballot_sync(kFull, has);
+            if (!m) return;
+            uint32_t base = 0;
+            if (lane == 0) base = atomicAdd(&n_xedges, (uint32_t)__popc(m));
+            base = __shfl_sync(kFull, base, 0);
+            if (!has) return;
+            const uint32_t slot = base + __popc(m & ((1u << lane) - 1u));
             if (slot < xcap) {
                 XL[2 * slot] = x;
                 XL[2 * slot + 1] = y;
@@ -581,13 +609,13 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
                 uf.unite(x, y);
             }
         };
-        for (int c = tid; c < W; c += kFastThreads) {
+        for (int cbase = warp * 32; cbase < WPR * 32; cbase += kFastThreads) {
+            const int c = cbase + lane;
             const int cw = c >> 5, b = c & 31;
             const uint32_t uw = U[cw];
-            if (!((uw >> b) & 1u)) continue;
             const uint32_t upb = b > 0 ? (uw >> (b - 1)) & 1u : (cw > 0 ? U[cw - 1] >> 31 : 0u);
-            if (upb && ((L[cw] >> b) & 1u) && ((Lh[cw] >> b) & 1u)) continue;   // redundant
-            xpush(band | run_of(SB, NB, cw, b), bandu | run_of(SBu, NBu, wu0 + cw, b));
+            const bool has = ((uw >> b) & 1u) && !(upb && ((L[cw] >> b) & 1u) && ((Lh[cw] >> b) & 1u));
+            xpush(has, has ? band | run_of(SB, NB, cw, b) : 0u, has ? bandu | run_of(SBu, NBu, wu0 + cw, b) : 0u);
         }
         for (int o = 0; o < a.n_off; ++o) {
             const int dy = a.dy[o];
@@ -597,16 +625,16 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
                 if (tr < 0) continue;
                 const int kt = tr / R, tq = tr - kt * R;
                 const uint32_t *SBt = cl.map_shared_rank(SB, kt), *NBt = cl.map_shared_rank(NB, kt);
-                for (int c = tid; c < W; c += kFastThreads) {
+                for (int cbase = warp * 32; cbase < WPR * 32; cbase += kFastThreads) {
+                    const int c = cbase + lane;
                     const int cw = c >> 5, b = c & 31, w = q * WPR + cw;
                     const uint32_t m = M[w];
-                    if (!((m >> b) & 1u)) continue;
                     const uint32_t mpb = b > 0 ? (m >> (b - 1)) & 1u : (cw > 0 ? M[w - 1] >> 31 : 0u);
-                    if (mpb && ((L[w] >> b) & 1u) && ((T[w] >> b) & 1u)) continue;
+                    const bool has = c < W && ((m >> b) & 1u) && !(mpb && ((L[w] >> b) & 1u) && ((T[w] >> b) & 1u));
                     int tc = (c - a.dx[o]) % W;
                     if (tc < 0) tc += W;
-                    xpush(band | run_of(SB, NB, w, b),
-                          ((uint32_t)kt << a.SHN) | run_of(SBt, NBt, tq * WPR + tc / 32, tc & 31));
+                    xpush(has, has ? band | run_of(SB, NB, w, b) : 0u,
+                          has ? ((uint32_t)kt << a.SHN) | run_of(SBt, NBt, tq * WPR + tc / 32, tc & 31) : 0u);
                 }
             }
         }
@@ -614,6 +642,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
         const uint32_t nx = min(n_xedges, xcap);
         for (uint32_t e = tid; e < nx; e += kFastThreads) uf.unite(XL[2 * e], XL[2 * e + 1]);
     }
+    if (a.stop_after == 5) { cl.sync(); return; }
     RS_MARK(8);
     cl.sync();   // #2: the forest is final
     RS_MARK(9);
@@ -633,6 +662,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
         const uint32_t p = E[id];
         E[id] = ((p >> a.SHN) == (uint32_t)k) ? E[p & maskN] : uf.find_nc(p);
     }
+    if (a.stop_after == 6) { cl.sync(); return; }
     RS_MARK(10);
     cl.sync();   // #3: sizes are final at every root
 
@@ -717,6 +747,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
             }
         }
     }
+    if (a.stop_after == 7) { cl.sync(); return; }
     RS_MARK(12);
     cl.sync();   // #5: root labels are published
 
@@ -725,28 +756,33 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
         const uint32_t g = E[id];
         if (g != (band | id)) SZ[id] = *reinterpret_cast<volatile uint32_t *>(uf.slot(SZ, g));
     }
+    if (a.stop_after == 8) { cl.sync(); return; }
     RS_MARK(13);
     cl.sync();   // #6: no DSMEM access after this point
 
     RS_MARK(14);
     int32_t *out = a.labels + (size_t)frame * H * W + (size_t)r0 * W;
-    if ((W & 3) == 0) {
-        // lane handles 4 consecutive cells of a word: 16-byte streaming stores
-        for (int g4 = warp; g4 * 4 < nw; g4 += kFastWarps) {
-            const int w = g4 * 4 + (lane >> 3);
-            if (w >= nw) continue;
-            const int q = divWPR(a, w);
-            const int cw = w - q * WPR;
-            const int b0 = (lane & 7) * 4;
-            const int c = cw * 32 + b0;
-            if (c >= W) continue;
-            const uint32_t pw = P[w] >> b0, sbw = SB[w], nbw = NB[w];
+    if ((WPR & 3) == 0 && (W & 31) == 0) {
+        // rows are whole words, so cell index == 32 * word + bit: a linear
+        // sweep, lane = 4 consecutive cells, 16-byte streaming stores; run
+        // ids of the lane's cells are the first id plus the run starts after it
+        const int b0 = (lane & 7) * 4;
+        const uint32_t lem = lanemask_le(b0);
+        const uint32_t *SZc = SZ;
+        for (int w0 = warp * 4; w0 < nw; w0 += kFastWarps * 4) {
+            const int w = w0 + (lane >> 3);
+            const uint32_t pw = P[w] >> b0, sbw = SB[w];
+            const uint32_t id0 = NB[w] + __popc(sbw & lem) - 1u;
+            const uint32_t st = sbw >> b0;
+            const uint32_t id1 = id0 + ((st >> 1) & 1u);
+            const uint32_t id2 = id1 + ((st >> 2) & 1u);
+            const uint32_t id3 = id2 + ((st >> 3) & 1u);
             int4 lab;
-            int *lp = &lab.x;
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-                lp[j] = ((pw >> j) & 1u) ? (int)SZ[nbw + __popc(sbw & lanemask_le(b0 + j)) - 1u] : 0;
-            __stcs(reinterpret_cast<int4 *>(out + q * W + c), lab);
+            lab.x = (pw & 1u) ? (int)SZc[id0] : 0;
+            lab.y = (pw & 2u) ? (int)SZc[id1] : 0;
+            lab.z = (pw & 4u) ? (int)SZc[id2] : 0;
+            lab.w = (pw & 8u) ? (int)SZc[id3] : 0;
+            __stcs(reinterpret_cast<int4 *>(out + w0 * 32 + lane * 4), lab);
         }
     } else {
         for (int w = warp; w < nw; w += kFastWarps) {
