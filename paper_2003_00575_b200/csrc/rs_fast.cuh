@@ -517,9 +517,12 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
             const uint32_t id = base + lane;
             bool lr = false;
             if (id < n_runs) {
-                // path halving with atomicMin: entries only ever decrease, so a
-                // finished root pointer (the tree minimum) is never overwritten
-                const uint32_t r = uf.find_local_min(band | id);
+                // most trees are at most two deep after the unions: two plain
+                // loads, then (rarely) path halving with atomicMin — entries only
+                // ever decrease, so a finished root pointer is never overwritten
+                const uint32_t p = E[id];
+                const uint32_t gp = E[p & maskN];
+                const uint32_t r = gp == p ? p : uf.find_local_min(gp);
                 E[id] = r;
                 SZ[id] = 0;   // it served as the edge list
                 lr = r == (band | id);
@@ -657,6 +660,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
         }
     }
     __syncthreads();
+#pragma unroll 4
     for (uint32_t id = tid; id < n_runs; id += kFastThreads) {
         if ((LR[id >> 5] >> (id & 31)) & 1u) continue;
         const uint32_t p = E[id];
@@ -734,6 +738,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
     {
         const uint32_t prefix = cta_prefix;
         const uint32_t *WK = LR;
+#pragma unroll 4
         for (uint32_t id = tid; id < n_runs; id += kFastThreads) {
             if (E[id] != (band | id)) continue;
             const uint32_t km = KB[id >> 5];
@@ -752,9 +757,11 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
     cl.sync();   // #5: root labels are published
 
     // ---- L. run labels, then cell labels -----------------------------------
+    // root labels are final after barrier #5: plain (batchable) DSMEM loads
+#pragma unroll 4
     for (uint32_t id = tid; id < n_runs; id += kFastThreads) {
         const uint32_t g = E[id];
-        if (g != (band | id)) SZ[id] = *reinterpret_cast<volatile uint32_t *>(uf.slot(SZ, g));
+        if (g != (band | id)) SZ[id] = *uf.slot(SZ, g);
     }
     if (a.stop_after == 8) { cl.sync(); return; }
     RS_MARK(13);
