@@ -42,14 +42,25 @@ struct KArgs {
 };
 
 // ------------------------------------------------------------ phase markers
-constexpr int kProfSlots = 16;
+constexpr int kProfSlots = 20;   // 16 clock64 marks, [16] start / [17] end globaltimer, [18] SM id
 constexpr int kProfCtas = 8192;
 #ifdef RS_PHASE_PROF
 __device__ long long g_prof[kProfCtas * kProfSlots];
 #define RS_MARK(i)                                                             \
     do {                                                                       \
-        if (threadIdx.x == 0 && blockIdx.x < kProfCtas)                        \
+        if (threadIdx.x == 0 && blockIdx.x < kProfCtas) {                      \
             ::rs::g_prof[blockIdx.x * kProfSlots + (i)] = clock64();           \
+            if ((i) == 0 || (i) == 15) {                                       \
+                unsigned long long gt;                                         \
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));         \
+                ::rs::g_prof[blockIdx.x * kProfSlots + 16 + ((i) == 15)] = gt; \
+            }                                                                  \
+            if ((i) == 0) {                                                    \
+                unsigned smid;                                                 \
+                asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));              \
+                ::rs::g_prof[blockIdx.x * kProfSlots + 18] = smid;             \
+            }                                                                  \
+        }                                                                      \
     } while (0)
 #else
 #define RS_MARK(i) \
@@ -104,18 +115,51 @@ __device__ __forceinline__ bool ground_rule(const KArgs &a, const GroundRow &g, 
     return ok && z <= a.keep_above;
 }
 
-// The same decision with the row constants in registers and the window test
-// as min(L,U) <= num <= max(L,U): lo <= hi and rounding is monotone, so
-// [L, U] is ordered for den > 0 and reversed for den < 0 — exactly the
-// reference's two branches; den == 0 fails either way.
-__device__ __forceinline__ bool ground_rule_mm(float mount, float keep, float sa, float ca, float lo, float hi,
-                                               float sc, float d1, float d2, float v) {
+// The height test z = v*sc + mount <= keep_above (two rounded ops) as one
+// product against a per-row threshold: both rounded ops are monotone in v, so
+// the cells passing are {v <= T} (sc > 0), {v >= T} (sc < 0) or all / none
+// (sc == 0, or no finite v at the boundary).  cond(v) == (v * zs <= zt) with
+// zs in {1, -1, 0}; T is found by bisection over float bit patterns with the
+// reference's exact ops.  Valid for finite v >= 0 (the range contract).
+__device__ __forceinline__ bool z_pass(float v, float sc, float mount, float keep) {
+    return __fadd_rn(__fmul_rn(v, sc), mount) <= keep;
+}
+
+__device__ inline void z_threshold(float sc, float mount, float keep, float &zs, float &zt) {
+    const float vmax = __int_as_float(0x7f7fffff);
+    const bool at0 = z_pass(0.f, sc, mount, keep), atmax = z_pass(vmax, sc, mount, keep);
+    if (!(sc > 0.f || sc < 0.f) || at0 == atmax) {   // constant over [0, FLT_MAX]
+        zs = 0.f;
+        zt = at0 ? 0.f : -1.f;
+        return;
+    }
+    // bisection: f(lo) == at0, f(hi) == atmax (they differ)
+    int lo = 0, hi = 0x7f7fffff;
+    while (hi - lo > 1) {
+        const int mid = lo + (hi - lo) / 2;
+        if (z_pass(__int_as_float(mid), sc, mount, keep) == at0) lo = mid; else hi = mid;
+    }
+    if (at0) { zs = 1.f; zt = __int_as_float(lo); }     // passes for v <= lo
+    else { zs = -1.f; zt = -__int_as_float(hi); }       // passes for v >= hi
+}
+
+// Ground decision for BitsStrip with the row constants in registers:
+//  * window: [L, U] = [lo, hi] * den is ordered for den > 0 and reversed for
+//    den < 0 (the reference's two branches); with |den| the bounds are
+//    |L|, |U| exactly (round-to-nearest is sign-symmetric) and the test is
+//    lo*|den| <= num*sign(den) <= hi*|den|; den == 0 fails either way;
+//  * only the partner range `other` needs the > 0 test: the cell's own range
+//    v > 0 is part of the presence predicate this result is combined with;
+//  * the height test is z_threshold's single product.
+__device__ __forceinline__ bool ground_fast(float sa, float ca, float lo, float hi, float zs, float zt, float d1,
+                                            float d2, float v, float other) {
     const float num = __fmul_rn(d2, sa);
     const float den = __fsub_rn(d1, __fmul_rn(d2, ca));
-    const float L = __fmul_rn(lo, den);
-    const float U = __fmul_rn(hi, den);
-    const float z = __fadd_rn(__fmul_rn(v, sc), mount);
-    return (fminf(L, U) <= num) & (num <= fmaxf(L, U)) & (den != 0.f) & (fminf(d1, d2) > 0.f) & (z <= keep);
+    const float ad = fabsf(den);
+    const float L = __fmul_rn(lo, ad);
+    const float U = __fmul_rn(hi, ad);
+    const float ns = __int_as_float(__float_as_int(num) ^ (__float_as_int(den) & 0x80000000));
+    return (L <= ns) & (ns <= U) & (den != 0.f) & (other > 0.f) & (__fmul_rn(v, zs) <= zt);
 }
 
 // Presence = valid && !ground for cell (r, c); `get(row, col)` returns the range.
@@ -140,6 +184,21 @@ __device__ __forceinline__ uint32_t lanemask_le(int lane) {
 
 __device__ __forceinline__ uint32_t smem_addr(const void *p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
+    uint32_t v;
+    asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+
+__device__ __forceinline__ void cp_async16(void *dst, const void *src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
 __device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {

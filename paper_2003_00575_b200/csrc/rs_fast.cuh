@@ -163,13 +163,13 @@ struct BitsStrip {
             else if (!FULL) x[j] = 0.f;
     }
 
-    // va = row above, v = this row, vb = row below; vn <- row r+2
-    template <bool ROW0>
+    // va = row above, v = this row, vb = row below; vn <- row r+2 (PF)
+    template <bool ROW0, bool PF = true>
     __device__ __forceinline__ void step(int r, const float (&va)[4], const float (&v)[4], const float (&vb)[4],
                                          float (&vn)[4], const uint32_t (&pin)[4], uint32_t (&pout)[4]) const {
-        ld4(r + 2, vn, r + 2 < rend);
+        if (PF) ld4(r + 2, vn, r + 2 < rend);
         const float4 c = *reinterpret_cast<const float4 *>(rowc + (r - rstart) * 8);
-        const float2 c2 = *reinterpret_cast<const float2 *>(rowc + (r - rstart) * 8 + 4);
+        const float4 c2 = *reinterpret_cast<const float4 *>(rowc + (r - rstart) * 8 + 4);
         const int srcl = (lane + 31) & 31;
         const bool last = lane == 31;
         uint32_t lw[4], uw[4];
@@ -177,7 +177,7 @@ struct BitsStrip {
         for (int j = 0; j < 4; ++j) {
             const float d1 = ROW0 ? v[j] : va[j];
             const float d2 = ROW0 ? vb[j] : v[j];
-            const bool gr = ground_on & ground_rule_mm(mount, keep, c.x, c.y, c.z, c.w, c2.x, d1, d2, v[j]);
+            const bool gr = ground_on & ground_fast(c.x, c.y, c.z, c.w, c2.x, c2.z, d1, d2, v[j], ROW0 ? vb[j] : va[j]);
             pout[j] = __ballot_sync(kFull, (v[j] > 0.f) & !gr);
             // left neighbour: lane l-1's cell; lane 0 reads lane 31's cell of
             // word j-1 (word 0 of the chunk: bit 0 is completed in step B)
@@ -288,7 +288,8 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
     for (int r = rstart + tid; r < rend; r += kFastThreads) {
         const GroundRow g = ground_row(a, r);
         float *rc = rowc + (r - rstart) * 8;
-        rc[0] = g.sa; rc[1] = g.ca; rc[2] = g.lo; rc[3] = g.hi; rc[4] = g.sc;
+        rc[0] = g.sa; rc[1] = g.ca; rc[2] = g.lo; rc[3] = g.hi;
+        z_threshold(g.sc, a.mount, a.keep_above, rc[4], rc[6]);
         rc[5] = r >= 1 ? __ldg(a.tables + 5 * H - 4 + r - 1) : 0.f;
     }
     __syncthreads();
@@ -296,10 +297,11 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
         const int nchunk = (W + 127) / 128;
         for (int ch = warp; ch < nchunk; ch += kFastWarps) {
             const int cb = ch * 128 + lane;
-            if (ch * 128 + 128 <= W && (WPR & 3) == 0)
-                BitsStrip<true>{a, fr + cb, rowc, P, L, U, Ph, Lh, ch, lane, r0, rstart, rend, cb,
-                                thr, tch, a.mount, a.keep_above, a.ground != 0}.run();
-            else
+            if (ch * 128 + 128 <= W && (WPR & 3) == 0) {
+                const BitsStrip<true> bs{a, fr + cb, rowc, P, L, U, Ph, Lh, ch, lane, r0, rstart, rend, cb,
+                                         thr, tch, a.mount, a.keep_above, a.ground != 0};
+                bs.run();
+            } else
                 BitsStrip<false>{a, fr + cb, rowc, P, L, U, Ph, Lh, ch, lane, r0, rstart, rend, cb,
                                  thr, tch, a.mount, a.keep_above, a.ground != 0}.run();
         }
@@ -432,76 +434,108 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
     RunUF uf{E, cl, maskN, a.SHN, k};
     if (!overflow) {
         // ---- U. band-local unions ----------------------------------------------
-        // Edges are gathered into a list first so that all lanes unite in
-        // parallel (word-wise loops left ~6 of 32 lanes busy).  The size array
-        // is the buffer (zeroed again by the flatten below); an edge that does
-        // not fit is united on the spot — the union order never matters.
+        // Edges are gathered into a list (the size array is the buffer; it is
+        // zeroed again by the flatten below).  Then, with no finds at all,
+        // every run hooks under its smallest neighbour (atomicMin on its own
+        // entry: an acyclic forest since pointers go to smaller ids), the
+        // forest is flattened by a read-only chase, and finally all listed
+        // edges are united — by then almost all of them are already inside one
+        // tree and cost two loads.  A list that overflowed is re-gathered with
+        // the unions done on the spot (the union order never matters).
         uint32_t *EL = SZ;
         const uint32_t cap = (uint32_t)a.NC;
-        for (int wb = warp * 32; wb < nw; wb += kFastThreads) {
-            const int w = wb + lane;
-            const bool act = w < nw;
-            const int q = act ? divWPR(a, w) : 0;
-            const int cw = w - q * WPR;
-            const uint32_t lw = act ? L[w] : 0u, sb = act ? SB[w] : 0u, uw = act ? U[w] : 0u;
-            const bool pseudo = (sb & lw & 1u) != 0;
-            uint32_t nru = 0;
-            if (q > 0 && uw) {
-                const uint32_t uprev = (uw << 1) | (cw > 0 ? U[w - 1] >> 31 : 0u);
-                nru = uw & ~(uprev & lw & L[w - WPR]);
-            }
-            const bool sm_ = act && cw == 0 && ((seam[q >> 5] >> (q & 31)) & 1u);
-            uint32_t k = (uint32_t)pseudo + __popc(nru) + (uint32_t)sm_;
-            for (int o = 0; o < a.n_off && act; ++o) {
-                if (q < a.dy[o]) continue;   // partner above the band: step X
-                const uint32_t *M = MC + o * a.nwords;
-                const uint32_t m = M[w];
-                const uint32_t mprev = (m << 1) | (cw > 0 ? M[w - 1] >> 31 : 0u);
-                k += __popc(m & ~(mprev & lw & TL[o * a.nwords + w]));
-            }
-            // warp-aggregated reservation in the edge list
-            uint32_t inc = k;
-            for (int off = 1; off < 32; off <<= 1) {
-                const uint32_t t = __shfl_up_sync(kFull, inc, off);
-                if (lane >= off) inc += t;
-            }
-            uint32_t wbase = 0;
-            if (lane == 31 && inc) wbase = atomicAdd(&n_edges, inc);
-            wbase = __shfl_sync(kFull, wbase, 31);
-            if (!k) continue;
-            uint32_t slot = wbase + inc - k;
-            auto push = [&](uint32_t x, uint32_t y) {
-                if (slot < cap) EL[slot] = (x << 16) | y;
-                else uf.unite_local(band | x, band | y);
-                ++slot;
-            };
-            if (pseudo) push(run_of(SB, NB, w, 0), run_of(SB, NB, w - 1, 31));
-            for (; nru; nru &= nru - 1) {
-                const int b = __ffs(nru) - 1;
-                push(run_of(SB, NB, w, b), run_of(SB, NB, w - WPR, b));
-            }
-            if (sm_) push(run_of(SB, NB, w, 0), run_of(SB, NB, q * WPR + (W - 1) / 32, (W - 1) & 31));
-            for (int o = 0; o < a.n_off; ++o) {
-                const int dy = a.dy[o];
-                if (q < dy) continue;
-                const uint32_t *M = MC + o * a.nwords;
-                const uint32_t m = M[w];
-                const uint32_t mprev = (m << 1) | (cw > 0 ? M[w - 1] >> 31 : 0u);
-                for (uint32_t nr = m & ~(mprev & lw & TL[o * a.nwords + w]); nr; nr &= nr - 1) {
-                    const int b = __ffs(nr) - 1;
-                    int tc = (cw * 32 + b - a.dx[o]) % W;
-                    if (tc < 0) tc += W;
-                    push(run_of(SB, NB, w, b), run_of(SB, NB, (q - dy) * WPR + tc / 32, tc & 31));
+        auto gather = [&](const bool direct) {
+            for (int wb = warp * 32; wb < nw; wb += kFastThreads) {
+                const int w = wb + lane;
+                const bool act = w < nw;
+                const int q = act ? divWPR(a, w) : 0;
+                const int cw = w - q * WPR;
+                const uint32_t lw = act ? L[w] : 0u, sb = act ? SB[w] : 0u, uw = act ? U[w] : 0u;
+                const bool pseudo = (sb & lw & 1u) != 0;
+                uint32_t nru = 0;
+                if (q > 0 && uw) {
+                    const uint32_t uprev = (uw << 1) | (cw > 0 ? U[w - 1] >> 31 : 0u);
+                    nru = uw & ~(uprev & lw & L[w - WPR]);
+                }
+                const bool sm_ = act && cw == 0 && ((seam[q >> 5] >> (q & 31)) & 1u);
+                uint32_t k = (uint32_t)pseudo + __popc(nru) + (uint32_t)sm_;
+                for (int o = 0; o < a.n_off && act; ++o) {
+                    if (q < a.dy[o]) continue;   // partner above the band: step X
+                    const uint32_t *M = MC + o * a.nwords;
+                    const uint32_t m = M[w];
+                    const uint32_t mprev = (m << 1) | (cw > 0 ? M[w - 1] >> 31 : 0u);
+                    k += __popc(m & ~(mprev & lw & TL[o * a.nwords + w]));
+                }
+                uint32_t slot = 0;
+                if (!direct) {
+                    // warp-aggregated reservation in the edge list
+                    uint32_t inc = k;
+                    for (int off = 1; off < 32; off <<= 1) {
+                        const uint32_t t = __shfl_up_sync(kFull, inc, off);
+                        if (lane >= off) inc += t;
+                    }
+                    uint32_t wbase = 0;
+                    if (lane == 31 && inc) wbase = atomicAdd(&n_edges, inc);
+                    wbase = __shfl_sync(kFull, wbase, 31);
+                    slot = wbase + inc - k;
+                }
+                if (!k) continue;
+                auto push = [&](uint32_t x, uint32_t y) {
+                    if (direct) uf.unite_local(band | x, band | y);
+                    else if (slot < cap) EL[slot] = (x << 16) | y;
+                    ++slot;
+                };
+                if (pseudo) push(run_of(SB, NB, w, 0), run_of(SB, NB, w - 1, 31));
+                for (; nru; nru &= nru - 1) {
+                    const int b = __ffs(nru) - 1;
+                    push(run_of(SB, NB, w, b), run_of(SB, NB, w - WPR, b));
+                }
+                if (sm_) push(run_of(SB, NB, w, 0), run_of(SB, NB, q * WPR + (W - 1) / 32, (W - 1) & 31));
+                for (int o = 0; o < a.n_off; ++o) {
+                    const int dy = a.dy[o];
+                    if (q < dy) continue;
+                    const uint32_t *M = MC + o * a.nwords;
+                    const uint32_t m = M[w];
+                    const uint32_t mprev = (m << 1) | (cw > 0 ? M[w - 1] >> 31 : 0u);
+                    for (uint32_t nr = m & ~(mprev & lw & TL[o * a.nwords + w]); nr; nr &= nr - 1) {
+                        const int b = __ffs(nr) - 1;
+                        int tc = (cw * 32 + b - a.dx[o]) % W;
+                        if (tc < 0) tc += W;
+                        push(run_of(SB, NB, w, b), run_of(SB, NB, (q - dy) * WPR + tc / 32, tc & 31));
+                    }
                 }
             }
-        }
+        };
+        gather(false);
         __syncthreads();
         if (a.stop_after == 9) { cl.sync(); return; }
-        {
-            // contiguous slices per thread: edges next to each other in the list
-            // mostly join the same components, so neighbouring threads taking
-            // neighbouring edges would contend on the same roots
-            const uint32_t ne = min(n_edges, cap);
+        const uint32_t ne = n_edges;   // block-uniform
+        if (ne > cap) {
+            gather(true);
+        } else {
+            // hook every run under its smallest listed neighbour
+            for (uint32_t e = tid; e < ne; e += kFastThreads) {
+                const uint32_t x = EL[e], u = x >> 16, v = x & 0xffffu;
+                atomicMin(E + max(u, v), band | min(u, v));
+            }
+            __syncthreads();
+            // flatten the forest: read-only chase; other threads only ever
+            // store roots, which are ancestors, so a racing read is still valid
+            {
+                volatile uint32_t *V = E;
+                for (uint32_t id = tid; id < n_runs; id += kFastThreads) {
+                    uint32_t r = V[id];
+                    while (true) {
+                        const uint32_t rr = V[r & maskN];
+                        if (rr == r) break;
+                        r = rr;
+                    }
+                    V[id] = r;
+                }
+            }
+            __syncthreads();
+            // contiguous slices per thread: edges next to each other in the
+            // list mostly join the same components
             const uint32_t per = (ne + kFastThreads - 1) / kFastThreads;
             const uint32_t e0 = min(tid * per, ne), e1 = min(e0 + per, ne);
             for (uint32_t e = e0; e < e1; ++e) {
@@ -775,21 +809,25 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
         // ids of the lane's cells are the first id plus the run starts after it
         const int b0 = (lane & 7) * 4;
         const uint32_t lem = lanemask_le(b0);
-        const uint32_t *SZc = SZ;
-        for (int w0 = warp * 4; w0 < nw; w0 += kFastWarps * 4) {
+        // byte addresses in shared memory: one add per cell instead of an
+        // index → address computation per load
+        const uint32_t szb = smem_addr(SZ) - 4u;
+        int4 *dst = reinterpret_cast<int4 *>(out) + warp * 32 + lane;
+#pragma unroll 2
+        for (int w0 = warp * 4; w0 < nw; w0 += kFastWarps * 4, dst += kFastWarps * 32) {
             const int w = w0 + (lane >> 3);
             const uint32_t pw = P[w] >> b0, sbw = SB[w];
-            const uint32_t id0 = NB[w] + __popc(sbw & lem) - 1u;
             const uint32_t st = sbw >> b0;
-            const uint32_t id1 = id0 + ((st >> 1) & 1u);
-            const uint32_t id2 = id1 + ((st >> 2) & 1u);
-            const uint32_t id3 = id2 + ((st >> 3) & 1u);
+            uint32_t ad = szb + 4u * (NB[w] + __popc(sbw & lem));
             int4 lab;
-            lab.x = (pw & 1u) ? (int)SZc[id0] : 0;
-            lab.y = (pw & 2u) ? (int)SZc[id1] : 0;
-            lab.z = (pw & 4u) ? (int)SZc[id2] : 0;
-            lab.w = (pw & 8u) ? (int)SZc[id3] : 0;
-            __stcs(reinterpret_cast<int4 *>(out + w0 * 32 + lane * 4), lab);
+            lab.x = (pw & 1u) ? (int)lds_u32(ad) : 0;
+            ad += (st << 1) & 4u;
+            lab.y = (pw & 2u) ? (int)lds_u32(ad) : 0;
+            ad += st & 4u;
+            lab.z = (pw & 4u) ? (int)lds_u32(ad) : 0;
+            ad += (st >> 1) & 4u;
+            lab.w = (pw & 8u) ? (int)lds_u32(ad) : 0;
+            __stcs(dst, lab);
         }
     } else {
         for (int w = warp; w < nw; w += kFastWarps) {

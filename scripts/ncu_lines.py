@@ -28,3 +28,7 @@ print(f"total samples {tot_s}  total warp-instr {tot_i}")
 for s, n, ln, src, st in sorted(recs, reverse=True)[:top]:
     print(f"{ln:>5} {100*s/max(tot_s,1):5.1f}% smp {100*n/max(tot_i,1):5.1f}% ins | {src:70s} | " +
           " ".join(f"{k}:{v}" for v, k in st if v))
+if "--by-ins" in sys.argv:
+    print("--- by instructions")
+    for s, n, ln, src, st in sorted(recs, key=lambda t: -t[1])[:top]:
+        print(f"{ln:>5} {100*s/max(tot_s,1):5.1f}% smp {100*n/max(tot_i,1):5.1f}% ins | {src:70s}")

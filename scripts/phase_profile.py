@@ -35,7 +35,7 @@ torch.cuda.synchronize()
 ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
 ev[0].record(); pipe.segment_batch(frames); ev[1].record(); torch.cuda.synchronize()
 n = min(8192, a.batch * pipe.ctas_per_frame)
-buf = np.zeros((n, 16), dtype=np.int64)
+buf = np.zeros((n, 20), dtype=np.int64)
 _native.check(_native.lib().rs_phase_profile(buf.ctypes.data_as(ctypes.c_void_p), n))
 NM = len(names) + 1
 d = np.diff(buf[:, :NM], axis=1).astype(np.float64)
@@ -46,3 +46,12 @@ print(f"CTA lifetime cycles: mean {tot.mean():.0f} p50 {np.median(tot):.0f} p90 
 for i, nm in enumerate(names):
     print(f"  {nm:16s} mean {d[:, i].mean():9.0f}  p90 {np.percentile(d[:, i], 90):9.0f}  "
           f"share {100*d[:, i].mean()/tot.mean():5.1f}%")
+gs, ge = buf[:, 16], buf[:, 17]
+t0 = gs.min()
+print(f"globaltimer: start spread {(gs.max()-t0)/1e3:.1f} us, last end {(ge.max()-t0)/1e3:.1f} us, "
+      f"mean life {(ge-gs).mean()/1e3:.1f} us")
+order = np.argsort(gs)
+qs = [0, 0.1, 0.25, 0.5, 0.58, 0.75, 0.9, 1.0]
+print("start-time quantiles (us):", " ".join(f"{q:.2f}:{(np.quantile(gs, q)-t0)/1e3:.1f}" for q in qs))
+print("end-time quantiles (us):  ", " ".join(f"{q:.2f}:{(np.quantile(ge, q)-t0)/1e3:.1f}" for q in qs))
+print("distinct SMs used:", len(np.unique(buf[:, 18])))
