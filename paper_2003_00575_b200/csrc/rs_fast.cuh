@@ -163,31 +163,31 @@ struct BitsStrip {
             else if (!FULL) x[j] = 0.f;
     }
 
-    // va = row above, v = this row, vb = row below; vn <- row r+2 (PF)
+    // va = row above, v = this row, vb = row below; vn <- row r+2 (PF).
+    // Stores the raw ballots: presence P, left pair test EH (in the L plane)
+    // and up pair test EV (in the U plane); step B masks them with presence
+    // one word per thread, 32x cheaper than warp-uniform ops here.
     template <bool ROW0, bool PF = true>
     __device__ __forceinline__ void step(int r, const float (&va)[4], const float (&v)[4], const float (&vb)[4],
-                                         float (&vn)[4], const uint32_t (&pin)[4], uint32_t (&pout)[4]) const {
+                                         float (&vn)[4]) const {
         if (PF) ld4(r + 2, vn, r + 2 < rend);
         const float4 c = *reinterpret_cast<const float4 *>(rowc + (r - rstart) * 8);
         const float4 c2 = *reinterpret_cast<const float4 *>(rowc + (r - rstart) * 8 + 4);
         const int srcl = (lane + 31) & 31;
         const bool last = lane == 31;
-        uint32_t lw[4], uw[4];
+        uint32_t pw[4], lw[4], uw[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             const float d1 = ROW0 ? v[j] : va[j];
             const float d2 = ROW0 ? vb[j] : v[j];
             const bool gr = ground_on & ground_fast(c.x, c.y, c.z, c.w, c2.x, c2.z, d1, d2, v[j], ROW0 ? vb[j] : va[j]);
-            pout[j] = __ballot_sync(kFull, (v[j] > 0.f) & !gr);
+            pw[j] = __ballot_sync(kFull, (v[j] > 0.f) & !gr);
             // left neighbour: lane l-1's cell; lane 0 reads lane 31's cell of
-            // word j-1 (word 0 of the chunk: bit 0 is completed in step B)
+            // word j-1 (word 0 of the chunk: bit 0 is redone in step B)
             const float src = (j > 0 && last) ? v[j > 0 ? j - 1 : 0] : v[j];
             const float vl = __shfl_sync(kFull, src, srcl);
-            const uint32_t eh = __ballot_sync(kFull, pair_pass(vl, v[j], tch, thr));
-            const uint32_t ev = __ballot_sync(kFull, pair_pass(va[j], v[j], c2.y, thr));
-            const uint32_t pl = (pout[j] << 1) | (j > 0 ? pout[j > 0 ? j - 1 : 0] >> 31 : 0u);
-            lw[j] = eh & pout[j] & (j > 0 ? pl : pl & ~1u);
-            uw[j] = ROW0 ? 0u : (ev & pout[j] & pin[j]);
+            lw[j] = __ballot_sync(kFull, pair_pass(vl, v[j], tch, thr));
+            uw[j] = ROW0 ? 0u : __ballot_sync(kFull, pair_pass(va[j], v[j], c2.y, thr));
         }
         const bool halo = r < r0;
         const int cw = ch * 4;
@@ -195,12 +195,12 @@ struct BitsStrip {
             if (lane == 0) {
                 const int w = halo ? 0 : (r - r0) * a.WPR + cw;
                 uint32_t *dp = halo ? Ph + cw : P + w, *dl = halo ? Lh + cw : L + w;
-                *reinterpret_cast<uint4 *>(dp) = make_uint4(pout[0], pout[1], pout[2], pout[3]);
+                *reinterpret_cast<uint4 *>(dp) = make_uint4(pw[0], pw[1], pw[2], pw[3]);
                 *reinterpret_cast<uint4 *>(dl) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
                 if (!halo) *reinterpret_cast<uint4 *>(U + w) = make_uint4(uw[0], uw[1], uw[2], uw[3]);
             }
         } else if (lane < 4 && cw + lane < a.WPR) {
-            const uint32_t xp = lane == 0 ? pout[0] : lane == 1 ? pout[1] : lane == 2 ? pout[2] : pout[3];
+            const uint32_t xp = lane == 0 ? pw[0] : lane == 1 ? pw[1] : lane == 2 ? pw[2] : pw[3];
             const uint32_t xl = lane == 0 ? lw[0] : lane == 1 ? lw[1] : lane == 2 ? lw[2] : lw[3];
             const uint32_t xu = lane == 0 ? uw[0] : lane == 1 ? uw[1] : lane == 2 ? uw[2] : uw[3];
             if (halo) {
@@ -217,17 +217,14 @@ struct BitsStrip {
 
     __device__ __forceinline__ void run() const {
         float S0[4], S1[4], S2[4], S3[4];
-        uint32_t Q0[4] = {0u, 0u, 0u, 0u}, Q1[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) S0[j] = S1[j] = S2[j] = S3[j] = 0.f;
         int rf = rstart;
         if (rstart == 0) {   // row 0: ground pair (0, 1), no up edges
             ld4(0, S1);
             ld4(1, S2);
-            step<true>(0, S0, S1, S2, S3, Q0, Q1);
+            step<true>(0, S0, S1, S2, S3);
             rf = 1;
-#pragma unroll
-            for (int j = 0; j < 4; ++j) Q0[j] = Q1[j];
         }
         if (rf >= rend) return;
         if (rf >= 1) ld4(rf - 1, S0);
@@ -235,13 +232,13 @@ struct BitsStrip {
         ld4(rf + 1, S2, rf + 1 < rend);
         // the first row walked in a band > 0 is the halo row: no up bits needed
         for (int r = rf; r < rend; r += 4) {
-            step<false>(r, S0, S1, S2, S3, Q0, Q1);
+            step<false>(r, S0, S1, S2, S3);
             if (r + 1 >= rend) break;
-            step<false>(r + 1, S1, S2, S3, S0, Q1, Q0);
+            step<false>(r + 1, S1, S2, S3, S0);
             if (r + 2 >= rend) break;
-            step<false>(r + 2, S2, S3, S0, S1, Q0, Q1);
+            step<false>(r + 2, S2, S3, S0, S1);
             if (r + 3 >= rend) break;
-            step<false>(r + 3, S3, S0, S1, S2, Q1, Q0);
+            step<false>(r + 3, S3, S0, S1, S2);
         }
     }
 };
@@ -310,25 +307,35 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
     RS_MARK(1);
     if (a.stop_after == 1) { cl.sync(); return; }
 
-    // ---- B. word-boundary left bits, seam, Map Connection bits ---------------
+    // ---- B. edge words, seam, Map Connection bits ----------------------------
+    // L = EH & P & (P shifted in from the left), U = EV & P & (P of the row
+    // above); bit 0 of a chunk's first word (whose left cell step A did not
+    // see) is tested here.  Word nw.. = the halo row (P / L only).
     for (int w = tid; w < nw + WPR; w += kFastThreads) {
         int cw, r;
-        uint32_t *Lw, pw, pprev;
+        uint32_t *Lw, pw, pprev, pab = 0, *Uw = nullptr, ev = 0;
         if (w < nw) {
             const int q = divWPR(a, w);
             cw = w - q * WPR;
             r = r0 + q;
-            if ((cw & 3) != 0 || cw == 0) continue;   // set in A except at chunk starts
-            Lw = L + w; pw = P[w]; pprev = P[w - 1];
+            Lw = L + w; Uw = U + w; pw = P[w]; ev = U[w];
+            pab = q > 0 ? P[w - WPR] : (r0 > 0 ? Ph[cw] : 0u);
+            pprev = cw > 0 ? P[w - 1] : 0u;
         } else {
             if (r0 == 0) break;
             cw = w - nw;
             r = r0 - 1;
-            if ((cw & 3) != 0 || cw == 0) continue;
-            Lw = Lh + cw; pw = Ph[cw]; pprev = Ph[cw - 1];
+            Lw = Lh + cw; pw = Ph[cw];
+            pprev = cw > 0 ? Ph[cw - 1] : 0u;
         }
-        const int c = cw * 32;
-        if ((pw & 1u) && (pprev >> 31) && pair_pass(G(r, c - 1), G(r, c), tch, thr)) *Lw |= 1u;
+        uint32_t eh = *Lw;
+        if ((cw & 3) == 0) {
+            eh &= ~1u;
+            const int c = cw * 32;
+            if (cw > 0 && (pw & 1u) && (pprev >> 31) && pair_pass(G(r, c - 1), G(r, c), tch, thr)) eh |= 1u;
+        }
+        *Lw = eh & pw & ((pw << 1) | (pprev >> 31));
+        if (Uw) *Uw = ev & pw & pab;
     }
     if (W > 1) {
         for (int q = tid; q < rows; q += kFastThreads) {
