@@ -42,7 +42,7 @@ struct KArgs {
 };
 
 // ------------------------------------------------------------ phase markers
-constexpr int kProfSlots = 20;   // 16 clock64 marks, [16] start / [17] end globaltimer, [18] SM id
+constexpr int kProfSlots = 24;   // clock64 marks 0-15 and 19-23, [16] start / [17] end globaltimer, [18] SM id
 constexpr int kProfCtas = 8192;
 #ifdef RS_PHASE_PROF
 __device__ long long g_prof[kProfCtas * kProfSlots];

@@ -444,11 +444,12 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
         // Edges are gathered into a list (the size array is the buffer; it is
         // zeroed again by the flatten below).  Then, with no finds at all,
         // every run hooks under its smallest neighbour (atomicMin on its own
-        // entry: an acyclic forest since pointers go to smaller ids), the
-        // forest is flattened by a read-only chase, and finally all listed
-        // edges are united — by then almost all of them are already inside one
-        // tree and cost two loads.  A list that overflowed is re-gathered with
-        // the unions done on the spot (the union order never matters).
+        // entry: an acyclic forest since pointers go to smaller ids; about 9
+        // in 10 edges are then inside one tree), and finally all listed edges
+        // are united; path halving in those finds flattens the forest (a
+        // separate flatten pass cost more than it saved).  A list that
+        // overflowed is re-gathered with the unions done on the spot (the
+        // union order never matters).
         uint32_t *EL = SZ;
         const uint32_t cap = (uint32_t)a.NC;
         auto gather = [&](const bool direct) {
@@ -492,12 +493,19 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
                     else if (slot < cap) EL[slot] = (x << 16) | y;
                     ++slot;
                 };
-                if (pseudo) push(run_of(SB, NB, w, 0), run_of(SB, NB, w - 1, 31));
-                for (; nru; nru &= nru - 1) {
-                    const int b = __ffs(nru) - 1;
-                    push(run_of(SB, NB, w, b), run_of(SB, NB, w - WPR, b));
+                // run ids from register copies: NB[w] counts the runs before
+                // word w, so the run holding bit 31 of word w-1 is NB[w] - 1
+                const uint32_t nbw = NB[w];
+                const uint32_t x0 = nbw + (sb & 1u) - 1u;   // run of bit 0
+                if (pseudo) push(nbw, nbw - 1u);
+                if (nru) {
+                    const uint32_t sbu = SB[w - WPR], nbu = NB[w - WPR] - 1u, nbm = nbw - 1u;
+                    for (; nru; nru &= nru - 1) {
+                        const uint32_t le = 0xffffffffu >> (31 - (__ffs(nru) - 1));
+                        push(nbm + __popc(sb & le), nbu + __popc(sbu & le));
+                    }
                 }
-                if (sm_) push(run_of(SB, NB, w, 0), run_of(SB, NB, q * WPR + (W - 1) / 32, (W - 1) & 31));
+                if (sm_) push(x0, run_of(SB, NB, q * WPR + (W - 1) / 32, (W - 1) & 31));
                 for (int o = 0; o < a.n_off; ++o) {
                     const int dy = a.dy[o];
                     if (q < dy) continue;
@@ -515,6 +523,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
         };
         gather(false);
         __syncthreads();
+        RS_MARK(19);
         if (a.stop_after == 9) { cl.sync(); return; }
         const uint32_t ne = n_edges;   // block-uniform
         if (ne > cap) {
@@ -526,21 +535,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
                 atomicMin(E + max(u, v), band | min(u, v));
             }
             __syncthreads();
-            // flatten the forest: read-only chase; other threads only ever
-            // store roots, which are ancestors, so a racing read is still valid
-            {
-                volatile uint32_t *V = E;
-                for (uint32_t id = tid; id < n_runs; id += kFastThreads) {
-                    uint32_t r = V[id];
-                    while (true) {
-                        const uint32_t rr = V[r & maskN];
-                        if (rr == r) break;
-                        r = rr;
-                    }
-                    V[id] = r;
-                }
-            }
-            __syncthreads();
+            RS_MARK(20);
             // contiguous slices per thread: edges next to each other in the
             // list mostly join the same components
             const uint32_t per = (ne + kFastThreads - 1) / kFastThreads;

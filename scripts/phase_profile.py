@@ -35,7 +35,7 @@ torch.cuda.synchronize()
 ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
 ev[0].record(); pipe.segment_batch(frames); ev[1].record(); torch.cuda.synchronize()
 n = min(8192, a.batch * pipe.ctas_per_frame)
-buf = np.zeros((n, 20), dtype=np.int64)
+buf = np.zeros((n, 24), dtype=np.int64)
 _native.check(_native.lib().rs_phase_profile(buf.ctypes.data_as(ctypes.c_void_p), n))
 NM = len(names) + 1
 d = np.diff(buf[:, :NM], axis=1).astype(np.float64)
@@ -55,3 +55,8 @@ qs = [0, 0.1, 0.25, 0.5, 0.58, 0.75, 0.9, 1.0]
 print("start-time quantiles (us):", " ".join(f"{q:.2f}:{(np.quantile(gs, q)-t0)/1e3:.1f}" for q in qs))
 print("end-time quantiles (us):  ", " ".join(f"{q:.2f}:{(np.quantile(ge, q)-t0)/1e3:.1f}" for q in qs))
 print("distinct SMs used:", len(np.unique(buf[:, 18])))
+sub = [("gather", 3, 19), ("hook", 19, 20), ("unite", 20, 4)]
+ok = (buf[:, 19] > 0) & (buf[:, 20] > 0)
+for nm, i, j in sub:
+    d2 = (buf[ok, j] - buf[ok, i]).astype(np.float64)
+    print(f"  U.{nm:10s} mean {d2.mean():9.0f}  p90 {np.percentile(d2, 90):9.0f}")
