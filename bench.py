@@ -314,7 +314,7 @@ def run_b200(args):
         e2e = {"value": world * B / float(te.item()), "unit": "frames/s",
                "h2d_bytes_per_step": int(h_in.nbytes + pipe._tables_host.nbytes),
                "d2h_bytes_per_step": int(h_lab.nbytes + h_ncl.nbytes + h_sz.nbytes),
-               "path": "rs_segment_batch_host (C ABI), pinned host buffers, 2 streams"}
+               "path": "rs_segment_batch_host (C ABI), pinned host buffers, 4 streams, 16 MB chunks"}
         # e2e results must equal the device path
         assert np.array_equal(h_lab, labels.cpu().numpy()), "e2e labels differ from device path"
 

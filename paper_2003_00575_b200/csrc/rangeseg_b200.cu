@@ -421,9 +421,12 @@ struct HostCtx {
     float *d_ranges = nullptr, *d_tables = nullptr;
     int32_t *d_labels = nullptr, *d_ncl = nullptr;
     int64_t *d_sizes = nullptr;
-    int *d_ws[2] = {nullptr, nullptr};
+    // kHostStreams streams round-robin over chunks, so the host->device copy
+    // of chunk j+2 can run while chunk j is copied back (both copy engines busy)
+    static constexpr int kHostStreams = 4;
+    int *d_ws[kHostStreams] = {};
     size_t cap_frames = 0, cap_tables = 0, cap_sizes = 0, frame_cells = 0, cap_ws = 0;
-    cudaStream_t s[2] = {nullptr, nullptr};
+    cudaStream_t s[kHostStreams] = {};
     int device = -1;
 };
 HostCtx g_host;
@@ -506,18 +509,19 @@ int rs_segment_batch_host(const rs_config *cfg, const float *h_tables, const flo
     cudaEvent_t tables_ready;
     cudaEventCreateWithFlags(&tables_ready, cudaEventDisableTiming);
     cudaEventRecord(tables_ready, g_host.s[0]);
-    cudaStreamWaitEvent(g_host.s[1], tables_ready, 0);
-    const int chunk = std::max(1, std::min<int>(batch, std::max<int>(1, (int)((8u << 20) / (HW * 4)))));
+    for (int i = 1; i < HostCtx::kHostStreams; ++i) cudaStreamWaitEvent(g_host.s[i], tables_ready, 0);
+    // 16 MB of ranges per chunk (measured best of 2-64 MB on the headline batch)
+    const int chunk = std::max(1, std::min<int>(batch, std::max<int>(1, (int)((16u << 20) / (HW * 4)))));
     for (int b0 = 0, j = 0; b0 < batch; b0 += chunk, ++j) {
         const int nb = std::min(chunk, batch - b0);
-        cudaStream_t s = g_host.s[j & 1];
+        cudaStream_t s = g_host.s[j % HostCtx::kHostStreams];
         const size_t off = (size_t)b0 * HW;
         if ((st = cuda_check(cudaMemcpyAsync(g_host.d_ranges + off, h_ranges + off, nb * HW * 4,
                                              cudaMemcpyHostToDevice, s), "copy ranges")))
             break;
         st = segment_launch(pl, g_host.d_tables, g_host.d_ranges + off, nb, g_host.d_labels + off, g_host.d_ncl + b0,
                             h_cluster_sizes ? g_host.d_sizes + (size_t)b0 * sizes_stride : nullptr, sizes_stride,
-                            g_host.d_ws[j & 1], s);
+                            g_host.d_ws[j % HostCtx::kHostStreams], s);
         if (st) break;
         if ((st = cuda_check(cudaMemcpyAsync(h_labels + off, g_host.d_labels + off, nb * HW * 4,
                                              cudaMemcpyDeviceToHost, s), "copy labels")))
@@ -533,10 +537,13 @@ int rs_segment_batch_host(const rs_config *cfg, const float *h_tables, const flo
                              "copy sizes")))
             break;
     }
-    const int st0 = cuda_check(cudaStreamSynchronize(g_host.s[0]), "stream sync");
-    const int st1 = cuda_check(cudaStreamSynchronize(g_host.s[1]), "stream sync");
+    int sst = RS_OK;
+    for (auto &hs : g_host.s) {
+        const int e = cuda_check(cudaStreamSynchronize(hs), "stream sync");
+        if (!sst) sst = e;
+    }
     cudaEventDestroy(tables_ready);
-    return st ? st : (st0 ? st0 : st1);
+    return st ? st : sst;
 }
 
 int rs_phase_profile(int64_t *host_out, int32_t max_ctas) {
