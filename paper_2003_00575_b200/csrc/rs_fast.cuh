@@ -79,7 +79,12 @@ struct RunUF {
             e = p;
         }
     }
+    // cluster-wide union of two runs: one hop to their band-local roots
+    // (flattened in step U), then finds with path halving among roots only, so
+    // every other run keeps pointing at its band-local root (step L relies on it)
     __device__ void unite(uint32_t x, uint32_t y) const {
+        x = ld(x);
+        y = ld(y);
         while (true) {
             x = find(x);
             y = find(y);
@@ -246,7 +251,8 @@ struct BitsStrip {
 __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const __grid_constant__ KArgs a) {
     extern __shared__ __align__(128) uint32_t sm[];
     __shared__ uint32_t warp_tot[kFastWarps];
-    __shared__ uint32_t cta_cnt, cta_sum, cta_prefix, ovf, ovf_any, n_edges, n_xedges;
+    __shared__ uint32_t cta_cnt, cta_sum, ovf, ovf_any, n_edges, n_xedges;
+    __shared__ uint32_t cta_pre[16];   // label base of every band of the cluster
     __shared__ uint32_t seam[2];   // seam edge per own row (R <= 64)
     __shared__ __align__(16) float rowc[(64 + 1) * 8];   // per-row constants of the band
 
@@ -687,6 +693,8 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
     RS_MARK(9);
 
     // ---- Z. resolve: local roots chase their global root and add their size ---
+    // Only band-local roots move (E[lr] = global root); other runs keep their
+    // local root and resolve through it when labelled.
     for (uint32_t id = tid; id < n_runs; id += kFastThreads) {
         if (!((LR[id >> 5] >> (id & 31)) & 1u)) continue;
         const uint32_t g = uf.find_min(band | id);
@@ -694,13 +702,6 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
             E[id] = g;
             atomicAdd(uf.slot(SZ, g), SZ[id]);
         }
-    }
-    __syncthreads();
-#pragma unroll 4
-    for (uint32_t id = tid; id < n_runs; id += kFastThreads) {
-        if ((LR[id >> 5] >> (id & 31)) & 1u) continue;
-        const uint32_t p = E[id];
-        E[id] = ((p >> a.SHN) == (uint32_t)k) ? E[p & maskN] : uf.find_nc(p);
     }
     if (a.stop_after == 6) { cl.sync(); return; }
     RS_MARK(10);
@@ -755,53 +756,57 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
             WK[w] += warp_tot[min(w / max(wper, 1u), (uint32_t)kFastWarps - 1)];
     }
     RS_MARK(11);
-    cl.sync();   // #4: every band's kept count and kept-size sum are published
-    if (tid == 0) {
+    cl.sync();   // #4: every band's kept bits, word prefixes and counts are published
+    if (tid < a.C) {
+        // label base of each band: kept roots of the bands before it
         uint32_t pre = 0, tot = 0, sum = 0;
         for (int j = 0; j < a.C; ++j) {
             const uint32_t cj = *cl.map_shared_rank(&cta_cnt, j);
-            if (j < k) pre += cj;
+            if (j < tid) pre += cj;
             tot += cj;
-            sum += *cl.map_shared_rank(&cta_sum, j);
+            if (tid == 0) sum += *cl.map_shared_rank(&cta_sum, j);
         }
-        cta_prefix = pre;
-        if (k == 0) {
+        cta_pre[tid] = pre;
+        if (tid == 0 && k == 0) {
             if (a.ncl) a.ncl[frame] = (int32_t)tot;
             if (a.sizes) a.sizes[(size_t)frame * a.sizes_stride] = (int64_t)H * W - (int64_t)sum;
         }
     }
     __syncthreads();
+    if (a.stop_after == 7) { cl.sync(); return; }
+    RS_MARK(12);
+
+    // ---- L. run labels straight from the root's band: label = band base +
+    // kept roots before it (word prefix + bits below) + 1, or 0 if dropped.
+    // Kept bits and prefixes are final after barrier #4 (plain DSMEM loads).
     {
-        const uint32_t prefix = cta_prefix;
         const uint32_t *WK = LR;
 #pragma unroll 4
         for (uint32_t id = tid; id < n_runs; id += kFastThreads) {
-            if (E[id] != (band | id)) continue;
-            const uint32_t km = KB[id >> 5];
-            const uint32_t b = id & 31;
-            if ((km >> b) & 1u) {
-                const uint32_t label = prefix + WK[id >> 5] + __popc(km & ((1u << b) - 1u)) + 1u;
-                if (a.sizes) a.sizes[(size_t)frame * a.sizes_stride + label] = (int64_t)SZ[id];
-                SZ[id] = label;
+            const uint32_t lr = E[id];
+            const uint32_t g = ((lr >> a.SHN) == (uint32_t)k) ? E[lr & maskN] : lr;
+            const int owner = (int)(g >> a.SHN);
+            const uint32_t gi = g & maskN;
+            uint32_t km, wk;
+            if (owner == k) {
+                km = KB[gi >> 5];
+                wk = WK[gi >> 5];
             } else {
-                SZ[id] = 0;   // dropped by filter_small
+                km = *cl.map_shared_rank(KB + (gi >> 5), owner);
+                wk = *cl.map_shared_rank(WK + (gi >> 5), owner);
             }
+            const uint32_t b = gi & 31;
+            uint32_t label = 0;
+            if ((km >> b) & 1u) {
+                label = cta_pre[owner] + wk + __popc(km & ((1u << b) - 1u)) + 1u;
+                if (g == (band | id) && a.sizes) a.sizes[(size_t)frame * a.sizes_stride + label] = (int64_t)SZ[id];
+            }
+            SZ[id] = label;   // only this thread read SZ[id] (the root's size)
         }
-    }
-    if (a.stop_after == 7) { cl.sync(); return; }
-    RS_MARK(12);
-    cl.sync();   // #5: root labels are published
-
-    // ---- L. run labels, then cell labels -----------------------------------
-    // root labels are final after barrier #5: plain (batchable) DSMEM loads
-#pragma unroll 4
-    for (uint32_t id = tid; id < n_runs; id += kFastThreads) {
-        const uint32_t g = E[id];
-        if (g != (band | id)) SZ[id] = *uf.slot(SZ, g);
     }
     if (a.stop_after == 8) { cl.sync(); return; }
     RS_MARK(13);
-    cl.sync();   // #6: no DSMEM access after this point
+    cl.sync();   // #5: no DSMEM access after this point
 
     RS_MARK(14);
     int32_t *out = a.labels + (size_t)frame * H * W + (size_t)r0 * W;

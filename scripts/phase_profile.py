@@ -22,8 +22,8 @@ p.add_argument("--core", action="store_true")
 p.add_argument("--skip", type=int, default=0)
 p.add_argument("--rows", type=int, default=0)
 a = p.parse_args()
-names = ["A bits", "B fixup/MC", "R runs", "U unions", "U flatten", "U sizes", "cs1+ovf", "X cross",
-         "cs2", "Z resolve", "cs3+K kept", "cs4+assign", "cs5+runlabels", "cs6", "cell labels"]
+names = ["A bits", "B edges/MC", "R runs", "U unions", "U flatten", "U sizes", "cs1+ovf", "X cross",
+         "cs2", "Z resolve", "cs3+K kept", "cs4+prefix", "run labels", "cs5", "cell labels"]
 spec = synthetic.CONFIGS[a.config]
 frames = synthetic.make_batch(a.config, a.batch, device="cuda")
 cfg = (rs.PipelineConfig(mc_pattern=rs.skip_pattern(a.skip), ground_removal=False, min_cluster_points=1)
