@@ -159,6 +159,7 @@ struct BitsStrip {
     int ch, lane, r0, rstart, rend, cb;
     float thr, tch, mount, keep;
     bool ground_on;
+    int rfirst;   // first row walked (rstart, or a later row when rows are split between warps)
 
     __device__ __forceinline__ void ld4(int r, float (&x)[4], bool pred = true) const {
         const float *p = col + (size_t)r * a.W;
@@ -224,8 +225,8 @@ struct BitsStrip {
         float S0[4], S1[4], S2[4], S3[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) S0[j] = S1[j] = S2[j] = S3[j] = 0.f;
-        int rf = rstart;
-        if (rstart == 0) {   // row 0: ground pair (0, 1), no up edges
+        int rf = rfirst;
+        if (rfirst == 0) {   // row 0: ground pair (0, 1), no up edges
             ld4(0, S1);
             ld4(1, S2);
             step<true>(0, S0, S1, S2, S3);
@@ -297,16 +298,22 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
     }
     __syncthreads();
     {
+        // narrow frames: split each chunk's rows between S warps so that no
+        // warp idles (a part starts one row early for its row-above values)
         const int nchunk = (W + 127) / 128;
-        for (int ch = warp; ch < nchunk; ch += kFastWarps) {
+        const int nrow = rend - rstart;
+        const int S = max(1, min(kFastWarps / nchunk, nrow / 8));
+        const int per = (nrow + S - 1) / S;
+        for (int t = warp; t < nchunk * S; t += kFastWarps) {
+            const int ch = t % nchunk, part = t / nchunk;
+            const int rlo = rstart + part * per, rhi = min(rend, rlo + per);
             const int cb = ch * 128 + lane;
-            if (ch * 128 + 128 <= W && (WPR & 3) == 0) {
-                const BitsStrip<true> bs{a, fr + cb, rowc, P, L, U, Ph, Lh, ch, lane, r0, rstart, rend, cb,
-                                         thr, tch, a.mount, a.keep_above, a.ground != 0};
-                bs.run();
-            } else
-                BitsStrip<false>{a, fr + cb, rowc, P, L, U, Ph, Lh, ch, lane, r0, rstart, rend, cb,
-                                 thr, tch, a.mount, a.keep_above, a.ground != 0}.run();
+            if (ch * 128 + 128 <= W && (WPR & 3) == 0)
+                BitsStrip<true>{a, fr + cb, rowc, P, L, U, Ph, Lh, ch, lane, r0, rstart, rhi, cb,
+                                thr, tch, a.mount, a.keep_above, a.ground != 0, rlo}.run();
+            else
+                BitsStrip<false>{a, fr + cb, rowc, P, L, U, Ph, Lh, ch, lane, r0, rstart, rhi, cb,
+                                 thr, tch, a.mount, a.keep_above, a.ground != 0, rlo}.run();
         }
     }
     __syncthreads();
