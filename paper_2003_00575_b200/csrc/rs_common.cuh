@@ -133,8 +133,23 @@ __device__ inline void z_threshold(float sc, float mount, float keep, float &zs,
         zt = at0 ? 0.f : -1.f;
         return;
     }
-    // bisection: f(lo) == at0, f(hi) == atmax (they differ)
+    // The boundary is within a few ulps of (keep - mount) / sc: bracket it
+    // by walking ulps from that estimate (bit patterns of non-negative floats
+    // are ordered), then bisect whatever bracket remains.  Invariant:
+    // f(lo) == at0, f(hi) == atmax.
     int lo = 0, hi = 0x7f7fffff;
+    {
+        const double est = ((double)keep - (double)mount) / (double)sc;
+        int t = est <= 0.0 ? 0 : est >= 3.0e38 ? 0x7f7fffff : __float_as_int((float)est);
+        t = max(0, min(t, 0x7f7fffff));
+        for (int i = 0; i < 8; ++i) {
+            const int a = max(0, t - 1), b = min(0x7f7fffff, t + 1);
+            if (z_pass(__int_as_float(a), sc, mount, keep) == at0) lo = max(lo, a); else { hi = min(hi, a); t = a - 1; continue; }
+            if (z_pass(__int_as_float(b), sc, mount, keep) != at0) { hi = min(hi, b); break; }
+            lo = max(lo, b);
+            t = b + 1;
+        }
+    }
     while (hi - lo > 1) {
         const int mid = lo + (hi - lo) / 2;
         if (z_pass(__int_as_float(mid), sc, mount, keep) == at0) lo = mid; else hi = mid;
