@@ -152,6 +152,31 @@ def test_odd_shapes_vs_oracle(H, W, rng, cuda):
             _assert_frame(res, b, wl, ws)
 
 
+@pytest.mark.parametrize("keep", [None, -1e30, -50.0, -1.7, -0.25, 0.0, 0.3, 2.5, 1e30])
+def test_height_threshold_edges_vs_oracle(keep, rng, cuda):
+    """The kernel replaces z = v*sin + mount <= keep_above by one product
+    against a per-row threshold found by exact search (rs_common.cuh
+    z_threshold); check it on rows with positive, zero and negative sines and
+    on ranges from subnormal to huge, ground mask and labels against the
+    oracle (ground.py:112-140 restated)."""
+    H, W = 24, 256
+    # elevations +6 .. -17 deg in 1 deg steps: row 6 is exactly 0 deg (sin 0)
+    model = rs.SensorModel(6.0 - 1.0 * np.arange(H), 360.0 / W, 1.7, width=W)
+    frames = np.exp(rng.uniform(np.log(0.05), np.log(200.0), size=(3, H, W))).astype(np.float32)
+    frames[rng.random(frames.shape) < 0.15] = 0
+    frames[0, :, :8] = np.float32(1e-40)           # subnormal ranges
+    frames[0, :, 8:16] = np.float32(3e38)          # near FLT_MAX
+    frames[1] = np.float32(5.0)                    # flat ring: many ties at the bound
+    cfg = rs.PipelineConfig(ground=rs.GroundParams(theta_deg=12.0, keep_above_z=keep),
+                            min_cluster_points=1)
+    pipe, res = _run(model, cfg, frames)
+    g, _, _ = pipe.stage_masks(torch.as_tensor(frames).cuda())
+    for b in range(3):
+        wl, ws, wg, _, _ = oracle.segment_frame(frames[b], pipe.packed, stages=True)
+        assert np.array_equal(g[b].cpu().numpy(), wg)
+        _assert_frame(res, b, wl, ws)
+
+
 def test_empty_and_full_frames(cuda):
     model = synthetic.sensor_for(synthetic.CONFIGS[0])
     frames = np.zeros((3, 64, 2048), np.float32)
