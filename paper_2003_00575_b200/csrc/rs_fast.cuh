@@ -360,7 +360,10 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
     }
     if (a.n_off > 0) {
         // Pairs (r-dy, c-dx mod W) <-> (r, c), evaluated by the lower/right cell;
-        // TL = left edge of the partner (redundant-edge test).
+        // TL = left edge of the partner (redundant-edge test): the partner's L
+        // bit when its row is in the band or the halo row (L final after this
+        // barrier), else tested here.
+        __syncthreads();
         for (int w = warp; w < nw; w += kFastWarps) {
             const int q = divWPR(a, w);
             const int cw = w - q * WPR;
@@ -370,28 +373,30 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
             const bool p = inb && ((P[w] >> lane) & 1u);
             const float v = inb ? G(r, c) : 0.f;
             for (int o = 0; o < a.n_off; ++o) {
-                const int tr = r - a.dy[o];
+                const int tr = r - a.dy[o];   // warp-uniform
                 int tc = (c - a.dx[o]) % W;
                 if (tc < 0) tc += W;
                 const bool has = inb && tr >= 0;
-                auto part = [&](int col, bool &pt, float &vt) {
-                    vt = G(tr, col);
-                    if (tr >= r0)
-                        pt = (P[(tr - r0) * WPR + col / 32] >> (col & 31)) & 1u;
-                    else if (tr == r0 - 1)
-                        pt = (Ph[col / 32] >> (col & 31)) & 1u;
-                    else
-                        pt = present_at(a, tr, col, G);
-                };
-                bool pt = false;
-                float vt = 0.f;
-                if (has) part(tc, pt, vt);
-                bool ptl = __shfl_up_sync(kFull, pt, 1);
-                float vtl = __shfl_up_sync(kFull, vt, 1);
-                if (has && tc > 0 && c > 0 && lane == 0) part(tc - 1, ptl, vtl);
                 const float tco = __ldg(a.tables + 6 * H - 5 + o * H + max(tr, 0));
-                const bool mc = has && p && pt && pair_pass(vt, v, tco, thr);
-                const bool tl = has && c > 0 && tc > 0 && pt && ptl && pair_pass(vtl, vt, tch, thr);
+                bool mc = false, tl = false;
+                if (tr >= r0 - 1) {
+                    const uint32_t *Pt = tr >= r0 ? P + (tr - r0) * WPR : Ph;
+                    const uint32_t *Lt = tr >= r0 ? L + (tr - r0) * WPR : Lh;
+                    if (has) {
+                        const bool pt = (Pt[tc >> 5] >> (tc & 31)) & 1u;
+                        mc = p && pt && pair_pass(G(tr, tc), v, tco, thr);
+                        tl = (Lt[tc >> 5] >> (tc & 31)) & 1u;
+                    }
+                } else {
+                    bool pt = false, ptl = false;
+                    float vt = 0.f, vtl = 0.f;
+                    if (has) { vt = G(tr, tc); pt = present_at(a, tr, tc, G); }
+                    ptl = __shfl_up_sync(kFull, pt, 1);
+                    vtl = __shfl_up_sync(kFull, vt, 1);
+                    if (has && tc > 0 && c > 0 && lane == 0) { vtl = G(tr, tc - 1); ptl = present_at(a, tr, tc - 1, G); }
+                    mc = has && p && pt && pair_pass(vt, v, tco, thr);
+                    tl = has && c > 0 && tc > 0 && pt && ptl && pair_pass(vtl, vt, tch, thr);
+                }
                 const uint32_t mm = __ballot_sync(kFull, mc);
                 const uint32_t mt = __ballot_sync(kFull, tl);
                 if (lane == 0) {
