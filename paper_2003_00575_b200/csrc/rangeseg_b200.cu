@@ -115,11 +115,6 @@ size_t dense_layout(int R, int W, int n_off, KArgs *k) {
 }
 
 // ---- fast kernel layout ---------------------------------------------------------
-size_t fast_bits_words(int R, int W, int n_off) {
-    const int WPR = (W + 31) / 32, nwords = R * WPR;
-    return (size_t)5 * nwords + 2 * WPR + (size_t)2 * n_off * nwords;
-}
-
 size_t fast_layout(int R, int W, int n_off, int NC, KArgs *k) {
     const int WPR = (W + 31) / 32, nwords = R * WPR;
     const int ncw = (NC + 31) / 32;
@@ -225,6 +220,11 @@ int make_plan(const rs_config *cfg, Plan *pl) {
         if (smem_f > kSmemLimit) continue;
         fill_common(cfg, Rf, pl->kf);
         fast_layout(Rf, W, n_off, (int)NC, &pl->kf);
+        // Map Connection offsets whose partner row is at most two rows up and
+        // at most 31 columns to the left are tested in step A (registers)
+        for (int o = 0; o < n_off && pl->kf.n_aoff < 4; ++o)
+            if (cfg->offsets[o][0] <= 2 && cfg->offsets[o][1] >= 0 && cfg->offsets[o][1] <= 31)
+                pl->kf.aoff[pl->kf.n_aoff++] = o;
         pl->kf.NC = (int)NC;
         int SHN = 0;
         while ((1 << SHN) < NC) ++SHN;
@@ -249,16 +249,21 @@ int set_attrs(const Plan &pl) {
     if (dev != g_attr_device) {
         g_attr_device = dev;
         g_attr_smem_f = g_attr_smem_d = 0;
-        if ((st = cuda_check(cudaFuncSetAttribute(rs::rs_fast_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
+        if ((st = cuda_check(cudaFuncSetAttribute(rs::rs_fast_kernel<false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
                              "cudaFuncSetAttribute(fast, non-portable cluster)")) ||
+            (st = cuda_check(cudaFuncSetAttribute(rs::rs_fast_kernel<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
+                             "cudaFuncSetAttribute(fast/MC, non-portable cluster)")) ||
             (st = cuda_check(cudaFuncSetAttribute(rs::rs_dense_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
                              "cudaFuncSetAttribute(dense, non-portable cluster)")))
             return st;
     }
     if (pl.fast && pl.smem_f > g_attr_smem_f) {
-        if ((st = cuda_check(cudaFuncSetAttribute(rs::rs_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        if ((st = cuda_check(cudaFuncSetAttribute(rs::rs_fast_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                   (int)std::max(pl.smem_f, (size_t)48 * 1024)),
-                             "cudaFuncSetAttribute(fast, smem)")))
+                             "cudaFuncSetAttribute(fast, smem)")) ||
+            (st = cuda_check(cudaFuncSetAttribute(rs::rs_fast_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                  (int)std::max(pl.smem_f, (size_t)48 * 1024)),
+                             "cudaFuncSetAttribute(fast/MC, smem)")))
             return st;
         g_attr_smem_f = pl.smem_f;
     }
@@ -320,7 +325,11 @@ int segment_launch(const Plan &pl, const float *d_tables, const float *d_ranges,
     kf.sizes_stride = sizes_stride;
     kf.ws = ws;
     kf.stop_after = pl.stop_after;
-    st = launch_cluster(rs::rs_fast_kernel, kf, batch, rs::kFastThreads, pl.smem_f, stream, "rs_fast_kernel launch");
+    st = kf.n_aoff > 0
+             ? launch_cluster(rs::rs_fast_kernel<true>, kf, batch, rs::kFastThreads, pl.smem_f, stream,
+                              "rs_fast_kernel launch")
+             : launch_cluster(rs::rs_fast_kernel<false>, kf, batch, rs::kFastThreads, pl.smem_f, stream,
+                              "rs_fast_kernel launch");
     if (st || !pl.may_overflow) return st;
     // Overflow pass: a few persistent clusters walk the (usually empty) list;
     // a programmatic dependent launch hides its launch latency behind the

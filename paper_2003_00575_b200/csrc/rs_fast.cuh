@@ -150,12 +150,12 @@ struct RunUF {
 // register moves.  Row 0 (whose ground pair is rows 0/1) is done by a
 // separate ROW0 step.  FULL: the chunk lies inside the row (no load guards,
 // 16-byte stores of the four words by lane 0).
-template <bool FULL>
+template <bool FULL, bool MCA>
 struct BitsStrip {
     const KArgs &a;
     const float *col;
     const float *rowc;
-    uint32_t *P, *L, *U, *Ph, *Lh;
+    uint32_t *P, *L, *U, *Ph, *Lh, *MCp;
     int ch, lane, r0, rstart, rend, cb;
     float thr, tch, mount, keep;
     bool ground_on;
@@ -176,6 +176,12 @@ struct BitsStrip {
     template <bool ROW0, bool PF = true>
     __device__ __forceinline__ void step(int r, const float (&va)[4], const float (&v)[4], const float (&vb)[4],
                                          float (&vn)[4]) const {
+        // MCA: vn still holds row r-2 until the prefetch below overwrites it
+        float v2[4];
+        if (MCA) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) v2[j] = vn[j];
+        }
         if (PF) ld4(r + 2, vn, r + 2 < rend);
         const float4 c = *reinterpret_cast<const float4 *>(rowc + (r - rstart) * 8);
         const float4 c2 = *reinterpret_cast<const float4 *>(rowc + (r - rstart) * 8 + 4);
@@ -197,6 +203,33 @@ struct BitsStrip {
         }
         const bool halo = r < r0;
         const int cw = ch * 4;
+        if (MCA && !halo) {
+            // raw pair tests of the step-A Map Connection offsets: partner
+            // (r - dy, c - dx) is lane l - dx of word j (or of word j-1 for
+            // l < dx: lanes 32-dx.. send their word j-1 value, as for the left
+            // neighbour); bits l < dx of the chunk's first word and all
+            // presence masking are done in step B
+            for (int i = 0; i < a.n_aoff; ++i) {
+                const int o = a.aoff[i], dy = a.dy[o], dx = a.dx[o];
+                const float tco = __ldg(a.tables + 6 * a.H - 5 + o * a.H + max(r - dy, 0));
+                const int sl = (lane - dx) & 31;
+                const bool prevw = lane >= 32 - dx;
+                uint32_t mw[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const float cur = dy == 0 ? v[j] : dy == 1 ? va[j] : v2[j];
+                    const float prv = j == 0 ? 0.f : (dy == 0 ? v[j > 0 ? j - 1 : 0] : dy == 1 ? va[j > 0 ? j - 1 : 0] : v2[j > 0 ? j - 1 : 0]);
+                    const float pv = __shfl_sync(kFull, (dx > 0 && prevw) ? prv : cur, sl);
+                    mw[j] = __ballot_sync(kFull, pair_pass(pv, v[j], tco, thr));
+                }
+                uint32_t *M = MCp + o * a.nwords + (r - r0) * a.WPR + cw;
+                if (FULL) {
+                    if (lane == 0) *reinterpret_cast<uint4 *>(M) = make_uint4(mw[0], mw[1], mw[2], mw[3]);
+                } else if (lane < 4 && cw + lane < a.WPR) {
+                    M[lane] = lane == 0 ? mw[0] : lane == 1 ? mw[1] : lane == 2 ? mw[2] : mw[3];
+                }
+            }
+        }
         if (FULL) {
             if (lane == 0) {
                 const int w = halo ? 0 : (r - r0) * a.WPR + cw;
@@ -236,6 +269,7 @@ struct BitsStrip {
         if (rf >= 1) ld4(rf - 1, S0);
         ld4(rf, S1);
         ld4(rf + 1, S2, rf + 1 < rend);
+        if (MCA && rf >= 2) ld4(rf - 2, S3);   // row r-2 of the first step (Map Connections)
         // the first row walked in a band > 0 is the halo row: no up bits needed
         for (int r = rf; r < rend; r += 4) {
             step<false>(r, S0, S1, S2, S3);
@@ -249,6 +283,10 @@ struct BitsStrip {
     }
 };
 
+// MCA: some Map Connection offsets (dy <= 2, 0 <= dx <= 31) are tested in
+// step A from the rows already in registers (a separate instantiation, so the
+// default kernel's code is untouched).
+template <bool MCA>
 __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const __grid_constant__ KArgs a) {
     extern __shared__ __align__(128) uint32_t sm[];
     __shared__ uint32_t warp_tot[kFastWarps];
@@ -309,11 +347,11 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
             const int rlo = rstart + part * per, rhi = min(rend, rlo + per);
             const int cb = ch * 128 + lane;
             if (ch * 128 + 128 <= W && (WPR & 3) == 0)
-                BitsStrip<true>{a, fr + cb, rowc, P, L, U, Ph, Lh, ch, lane, r0, rstart, rhi, cb,
-                                thr, tch, a.mount, a.keep_above, a.ground != 0, rlo}.run();
+                BitsStrip<true, MCA>{a, fr + cb, rowc, P, L, U, Ph, Lh, MC, ch, lane, r0, rstart, rhi, cb,
+                                     thr, tch, a.mount, a.keep_above, a.ground != 0, rlo}.run();
             else
-                BitsStrip<false>{a, fr + cb, rowc, P, L, U, Ph, Lh, ch, lane, r0, rstart, rhi, cb,
-                                 thr, tch, a.mount, a.keep_above, a.ground != 0, rlo}.run();
+                BitsStrip<false, MCA>{a, fr + cb, rowc, P, L, U, Ph, Lh, MC, ch, lane, r0, rstart, rhi, cb,
+                                      thr, tch, a.mount, a.keep_above, a.ground != 0, rlo}.run();
         }
     }
     __syncthreads();
@@ -364,16 +402,77 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
         // bit when its row is in the band or the halo row (L final after this
         // barrier), else tested here.
         __syncthreads();
-        for (int w = warp; w < nw; w += kFastWarps) {
+        RS_MARK(21);
+        auto is_aoff = [&](int o) {
+            bool hit = false;
+            if (MCA)
+                for (int i = 0; i < a.n_aoff; ++i) hit |= a.aoff[i] == o;
+            return hit;
+        };
+        if (MCA) {
+            // offsets tested in step A: mask the raw bits with the presence
+            // of both cells, partner left edges from the L plane, and redo the
+            // bits whose partner lies before the chunk (or across the seam);
+            // one word per thread
+            for (int i = 0; i < a.n_aoff; ++i) {
+                const int o = a.aoff[i], dy = a.dy[o], dx = a.dx[o];
+                uint32_t *M = MC + o * a.nwords, *T = TL + o * a.nwords;
+                for (int w = tid; w < nw; w += kFastThreads) {
+                    const int q = divWPR(a, w);
+                    const int cw = w - q * WPR;
+                    const int r = r0 + q, tr = r - dy;
+                    if (tr < r0 - 1 && tr >= 0) continue;   // partner above the halo row: below
+                    if (tr < 0) { M[w] = 0u; T[w] = 0u; continue; }
+                    const uint32_t *Pt = tr >= r0 ? P + (tr - r0) * WPR : Ph;
+                    const uint32_t *Lt = tr >= r0 ? L + (tr - r0) * WPR : Lh;
+                    const uint32_t pw = P[w];
+                    uint32_t pp = Pt[cw], tl = Lt[cw];
+                    if (dx > 0) {
+                        pp <<= dx;
+                        tl <<= dx;
+                        if (cw > 0) { pp |= Pt[cw - 1] >> (32 - dx); tl |= Lt[cw - 1] >> (32 - dx); }
+                    }
+                    uint32_t m = M[w] & pw & pp;
+                    if (dx > 0 && (cw & 3) == 0) {
+                        const uint32_t low = dx >= 32 ? kFull : ((1u << dx) - 1u);
+                        m &= ~low;
+                        tl &= ~low;
+                        const float tco = __ldg(a.tables + 6 * H - 5 + o * H + tr);
+                        for (int b = 0; b < dx && b < 32; ++b) {
+                            const int c = cw * 32 + b;
+                            if (c >= W) break;
+                            int tc = (c - dx) % W;
+                            if (tc < 0) tc += W;
+                            if ((Lt[tc >> 5] >> (tc & 31)) & 1u) tl |= 1u << b;
+                            if (((pw >> b) & 1u) && ((Pt[tc >> 5] >> (tc & 31)) & 1u) &&
+                                pair_pass(G(tr, tc), G(r, c), tco, thr))
+                                m |= 1u << b;
+                        }
+                    }
+                    M[w] = m;
+                    T[w] = tl;
+                }
+            }
+        }
+        RS_MARK(22);
+        // the per-lane path: every word for offsets not done in step A, and
+        // for those only the first dy-1 rows (partner above the halo row)
+        int wend = MCA ? 0 : nw;
+        for (int o = 0; o < a.n_off && wend < nw; ++o)
+            wend = max(wend, is_aoff(o) ? min(max(a.dy[o] - 1, 0), rows) * WPR : nw);
+        for (int w = warp; w < wend; w += kFastWarps) {
             const int q = divWPR(a, w);
             const int cw = w - q * WPR;
             const int c = cw * 32 + lane;
             const bool inb = c < W;
             const int r = r0 + q;
             const bool p = inb && ((P[w] >> lane) & 1u);
-            const float v = inb ? G(r, c) : 0.f;
+            float v = 0.f;
+            bool vload = false;
             for (int o = 0; o < a.n_off; ++o) {
                 const int tr = r - a.dy[o];   // warp-uniform
+                if (is_aoff(o) && !(tr < r0 - 1 && tr >= 0)) continue;   // done above
+                if (!vload) { v = inb ? G(r, c) : 0.f; vload = true; }
                 int tc = (c - a.dx[o]) % W;
                 if (tc < 0) tc += W;
                 const bool has = inb && tr >= 0;

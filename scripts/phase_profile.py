@@ -21,13 +21,16 @@ p.add_argument("--batch", type=int, default=256)
 p.add_argument("--core", action="store_true")
 p.add_argument("--skip", type=int, default=0)
 p.add_argument("--rows", type=int, default=0)
+p.add_argument("--offsets", default="", help="Map Connection offsets 'dy,dx;dy,dx' (overrides --skip)")
 a = p.parse_args()
 names = ["A bits", "B edges/MC", "R runs", "U unions", "U flatten", "U sizes", "cs1+ovf", "X cross",
          "cs2", "Z resolve", "cs3+K kept", "cs4+prefix", "run labels", "cs5", "cell labels"]
 spec = synthetic.CONFIGS[a.config]
 frames = synthetic.make_batch(a.config, a.batch, device="cuda")
-cfg = (rs.PipelineConfig(mc_pattern=rs.skip_pattern(a.skip), ground_removal=False, min_cluster_points=1)
-       if a.core else rs.PipelineConfig(mc_pattern=rs.skip_pattern(a.skip)))
+pat = (rs.MCPattern(tuple(tuple(int(x) for x in o.split(",")) for o in a.offsets.split(";")))
+       if a.offsets else rs.skip_pattern(a.skip))
+cfg = (rs.PipelineConfig(mc_pattern=pat, ground_removal=False, min_cluster_points=1)
+       if a.core else rs.PipelineConfig(mc_pattern=pat))
 pipe = rs.Pipeline(synthetic.sensor_for(spec), cfg, rows_per_cta=a.rows)
 for _ in range(3):
     pipe.segment_batch(frames)
@@ -60,3 +63,8 @@ ok = (buf[:, 19] > 0) & (buf[:, 20] > 0)
 for nm, i, j in sub:
     d2 = (buf[ok, j] - buf[ok, i]).astype(np.float64)
     print(f"  U.{nm:10s} mean {d2.mean():9.0f}  p90 {np.percentile(d2, 90):9.0f}")
+okb = (buf[:, 21] > 0) & (buf[:, 22] > 0)
+if okb.any():
+    for nm, i, j in [("B.edges+seam", 1, 21), ("B.step-A MC", 21, 22), ("B.other MC", 22, 2)]:
+        d3 = (buf[okb, j] - buf[okb, i]).astype(np.float64)
+        print(f"  {nm:14s} mean {d3.mean():9.0f}  p90 {np.percentile(d3, 90):9.0f}")

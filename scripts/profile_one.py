@@ -17,11 +17,14 @@ p.add_argument("--iters", type=int, default=3)
 p.add_argument("--skip", type=int, default=0)
 p.add_argument("--core", action="store_true")
 p.add_argument("--rows", type=int, default=0)
+p.add_argument("--offsets", default="", help="Map Connection offsets 'dy,dx;dy,dx' (overrides --skip)")
 a = p.parse_args()
 spec = synthetic.CONFIGS[a.config]
 frames = synthetic.make_batch(a.config, a.batch, device="cuda")
-cfg = (rs.PipelineConfig(mc_pattern=rs.skip_pattern(a.skip), ground_removal=False, min_cluster_points=1)
-       if a.core else rs.PipelineConfig(mc_pattern=rs.skip_pattern(a.skip)))
+pat = (rs.MCPattern(tuple(tuple(int(x) for x in o.split(",")) for o in a.offsets.split(";")))
+       if a.offsets else rs.skip_pattern(a.skip))
+cfg = (rs.PipelineConfig(mc_pattern=pat, ground_removal=False, min_cluster_points=1)
+       if a.core else rs.PipelineConfig(mc_pattern=pat))
 pipe = rs.Pipeline(synthetic.sensor_for(spec), cfg, rows_per_cta=a.rows)
 torch.cuda.synchronize()
 for _ in range(a.iters):

@@ -177,6 +177,28 @@ def test_height_threshold_edges_vs_oracle(keep, rng, cuda):
         _assert_frame(res, b, wl, ws)
 
 
+@pytest.mark.parametrize("H,W,rows", [(64, 2048, 0), (33, 300, 8), (40, 96, 16), (24, 4096, 0)])
+def test_step_a_map_connections_vs_oracle(H, W, rows, rng, cuda):
+    """Offsets with dy <= 2 and 0 <= dx <= 31 (at most four) are tested in
+    step A from registers (rs_fast.cuh, MCA): partners in the previous word,
+    before the chunk, across the azimuth seam and above the band, mixed with
+    offsets that take the per-lane path (dy >= 3, dx < 0, a fifth one)."""
+    model = _random_model(H, W)
+    frames = rng.uniform(0.5, 12.0, size=(3, H, W)).astype(np.float32)
+    frames[rng.random(frames.shape) < 0.25] = 0
+    frames[1] = 7.0                               # everything linked
+    frames[1, :, ::3] = 0
+    offs = ((0, 31), (1, 30), (2, 17), (0, 5), (2, 0), (3, 1), (1, -3))
+    offs = tuple(o for o in offs if o[0] < H and abs(o[1]) < W)
+    for cfg in (rs.PipelineConfig(ground_removal=False, min_cluster_points=1, mc_pattern=rs.MCPattern(offs)),
+                rs.PipelineConfig(ground_removal=False, min_cluster_points=3,
+                                  mc_pattern=rs.MCPattern(((0, 2), (2, 0))))):
+        pipe, res = _run(model, cfg, frames, rows_per_cta=rows)
+        for b in range(3):
+            wl, ws = oracle.segment_frame(frames[b], pipe.packed)
+            _assert_frame(res, b, wl, ws)
+
+
 def test_empty_and_full_frames(cuda):
     model = synthetic.sensor_for(synthetic.CONFIGS[0])
     frames = np.zeros((3, 64, 2048), np.float32)
