@@ -297,6 +297,40 @@ int launch_cluster(Kern kern, const KArgs &k, int clusters, int threads, size_t 
     return cuda_check(cudaLaunchKernelEx(&lc, kern, k), what);
 }
 
+// Clusters of the dense kernel that are co-resident in one wave: the
+// overflow pass uses that many persistent clusters, so a batch in which every
+// frame overflows still fills the GPU (an empty list costs the same).
+int dense_wave_clusters(const Plan &pl) {
+    static std::mutex mu;
+    static int dev_c = -1, C_c = 0, n_c = 0;
+    static size_t smem_c = 0;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 32 / pl.kd.C;
+    std::lock_guard<std::mutex> g(mu);
+    if (dev == dev_c && C_c == pl.kd.C && smem_c == pl.smem_d) return n_c;
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3((unsigned)pl.kd.C, 1, 1);
+    lc.blockDim = dim3((unsigned)rs::kDenseThreads, 1, 1);
+    lc.dynamicSmemBytes = pl.smem_d;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)pl.kd.C;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, rs::rs_dense_kernel, &lc) != cudaSuccess || n < 1) {
+        cudaGetLastError();
+        n = std::max(1, 32 / pl.kd.C);
+    }
+    dev_c = dev;
+    C_c = pl.kd.C;
+    smem_c = pl.smem_d;
+    n_c = n;
+    return n;
+}
+
 int segment_launch(const Plan &pl, const float *d_tables, const float *d_ranges, int32_t batch, int32_t *d_labels,
                    int32_t *d_n_clusters, int64_t *d_cluster_sizes, int64_t sizes_stride, int *ws,
                    cudaStream_t stream) {
@@ -335,7 +369,7 @@ int segment_launch(const Plan &pl, const float *d_tables, const float *d_ranges,
     // a programmatic dependent launch hides its launch latency behind the
     // fast kernel's tail.
     kd.list_mode = 1;
-    const int G = std::max(1, std::min<int>(batch, 32 / kd.C));
+    const int G = std::max(1, std::min<int>(batch, dense_wave_clusters(pl)));
     return launch_cluster(rs::rs_dense_kernel, kd, G, rs::kDenseThreads, pl.smem_d, stream,
                           "rs_dense_kernel (overflow) launch", true);
 }
