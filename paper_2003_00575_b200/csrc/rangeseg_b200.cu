@@ -226,6 +226,7 @@ int make_plan(const rs_config *cfg, Plan *pl) {
             if (cfg->offsets[o][0] <= 2 && cfg->offsets[o][1] >= 0 && cfg->offsets[o][1] <= 31)
                 pl->kf.aoff[pl->kf.n_aoff++] = o;
         pl->kf.NC = (int)NC;
+        pl->kf.udyn = pl->kf.C >= 4;
         int SHN = 0;
         while ((1 << SHN) < NC) ++SHN;
         pl->kf.SHN = SHN;

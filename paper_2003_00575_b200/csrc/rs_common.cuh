@@ -39,6 +39,7 @@ struct KArgs {
     int *ws;                      // [0] overflow count, [1] done counter, [2..] frame list
     int list_mode;                // dense kernel: process the overflow list
     int stop_after;               // experiments only: leave the fast kernel after phase N (0 = never)
+    int udyn;                     // fast kernel: dynamic edge grabbing in the local unions (clusters of >= 4 bands)
     int n_aoff;                   // Map Connection offsets evaluated in step A (dy <= 2, 0 <= dx <= 31), at most 4
     int aoff[4];                  // their indices into dy/dx
 };

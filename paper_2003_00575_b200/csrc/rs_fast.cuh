@@ -290,7 +290,7 @@ template <bool MCA>
 __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const __grid_constant__ KArgs a) {
     extern __shared__ __align__(128) uint32_t sm[];
     __shared__ uint32_t warp_tot[kFastWarps];
-    __shared__ uint32_t cta_cnt, cta_sum, ovf, ovf_any, n_edges, n_xedges;
+    __shared__ uint32_t cta_cnt, cta_sum, ovf, ovf_any, n_edges, n_xedges, ucur;
     __shared__ uint32_t cta_pre[16];   // label base of every band of the cluster
     __shared__ uint32_t seam[2];   // seam edge per own row (R <= 64)
     __shared__ __align__(16) float rowc[(64 + 1) * 8];   // per-row constants of the band
@@ -317,7 +317,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
     auto G = [&](int r, int c) -> float { return __ldg(fr + (size_t)r * W + c); };
 
     RS_MARK(0);
-    if (tid == 0) { seam[0] = seam[1] = 0; cta_sum = 0; n_edges = 0; n_xedges = 0; }
+    if (tid == 0) { seam[0] = seam[1] = 0; cta_sum = 0; n_edges = 0; n_xedges = 0; ucur = 0; }
 
     // ---- A. presence, left and up bits --------------------------------------
     // Row constants of the band (ground pair, height sine, vertical 2cos)
@@ -653,13 +653,30 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
             }
             __syncthreads();
             RS_MARK(20);
-            // contiguous slices per thread: edges next to each other in the
-            // list mostly join the same components
-            const uint32_t per = (ne + kFastThreads - 1) / kFastThreads;
-            const uint32_t e0 = min(tid * per, ne), e1 = min(e0 + per, ne);
-            for (uint32_t e = e0; e < e1; ++e) {
-                const uint32_t x = EL[e];
-                uf.unite_local(band | (x >> 16), band | (x & 0xffffu));
+            if (a.udyn) {
+                // many bands per frame (their loads differ the most): warps
+                // grab 256 edges at a time, 8 contiguous per lane
+                constexpr uint32_t kGrab = 8;
+                while (true) {
+                    uint32_t base = 0;
+                    if (lane == 0) base = atomicAdd(&ucur, 32 * kGrab);
+                    base = __shfl_sync(kFull, base, 0);
+                    if (base >= ne) break;
+                    const uint32_t e0 = min(base + lane * kGrab, ne), e1 = min(e0 + kGrab, ne);
+                    for (uint32_t e = e0; e < e1; ++e) {
+                        const uint32_t x = EL[e];
+                        uf.unite_local(band | (x >> 16), band | (x & 0xffffu));
+                    }
+                }
+            } else {
+                // contiguous slices per thread: edges next to each other in
+                // the list mostly join the same components
+                const uint32_t per = (ne + kFastThreads - 1) / kFastThreads;
+                const uint32_t e0 = min(tid * per, ne), e1 = min(e0 + per, ne);
+                for (uint32_t e = e0; e < e1; ++e) {
+                    const uint32_t x = EL[e];
+                    uf.unite_local(band | (x >> 16), band | (x & 0xffffu));
+                }
             }
         }
         __syncthreads();
