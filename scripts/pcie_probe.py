@@ -37,3 +37,17 @@ def both():
 t = timeit(h2d); print(f"H2D  {n / t / 1e9:6.1f} GB/s")
 t = timeit(d2h); print(f"D2H  {n / t / 1e9:6.1f} GB/s")
 t = timeit(both); print(f"both {2 * n / t / 1e9:6.1f} GB/s total ({t * 1e3:.2f} ms for {n >> 20} MiB each way)")
+
+
+def both_chunked(mb):
+    c = mb << 20
+    for o in range(0, n, c):
+        with torch.cuda.stream(s1):
+            d_in[o:o + c].copy_(h_in[o:o + c], non_blocking=True)
+        with torch.cuda.stream(s2):
+            h_out[o:o + c].copy_(d_out[o:o + c], non_blocking=True)
+
+
+for mb in (4, 16, 64):
+    t = timeit(lambda: both_chunked(mb))
+    print(f"both, {mb:2d} MiB chunks: {2 * n / t / 1e9:6.1f} GB/s total")
