@@ -31,7 +31,10 @@ namespace {
 constexpr int kMaxCluster = 16;
 constexpr int kMaxRowsPerCta = 31;            // dense kernel: seam bits of band + halo fit a word
 constexpr int kMaxRowsFast = 64;              // fast kernel: two seam words
-constexpr size_t kSmemLimit = 227 * 1024;     // per-CTA opt-in maximum on sm_100
+// per-CTA shared memory on sm_100 is at most 227 KB, static + dynamic: the
+// dynamic part of each kernel is capped below that by its static use
+// (fast kernel ~3.3 KB, dense kernel ~1.2 KB; rounded up)
+constexpr size_t kSmemLimit = 227 * 1024 - 4096;
 // kFastOcc fast CTAs per SM: 228 KB per SM, minus 1 KB reserved and the
 // static shared memory of each CTA
 constexpr size_t kFastSmemTarget = 228 * 1024 / rs::kFastOcc - 1024 - 2560;
