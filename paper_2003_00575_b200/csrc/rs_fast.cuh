@@ -5,27 +5,32 @@
 // so the azimuth seam is CTA-local.  Shared memory holds only bit planes and
 // per-run state, so two CTAs share an SM:
 //
-//   A  presence / left / up edge bits straight from global memory: each warp
-//      walks 32-column strips down the band, keeping the row above in
-//      registers and prefetching two rows ahead (the reference's float32
-//      rules, one rounding per op: ground.py:112-140, connectivity.py:47-92).
-//   B  word-boundary left bits, the seam, Map Connection bits.
+//   A  presence / left-pair / up-pair ballots straight from global memory:
+//      each warp walks a 128-column chunk down the band, keeping the row above
+//      in registers and prefetching two rows ahead (the reference's float32
+//      rules, one rounding per op: ground.py:112-140, connectivity.py:47-92);
+//      Map Connection offsets with dy <= 2, 0 <= dx <= 31 are tested here too
+//      (rs_fast_kernel<true>).
+//   B  presence masking of the edge words, chunk-boundary left bits, the
+//      seam, the remaining Map Connection bits.
 //   R  runs: start bits, and a block scan of their counts that numbers the
 //      runs of the band 0..n-1 in cell order (run id order == cell order).
-//   U  band-local union-find over run ids in shared memory (atomicMin hooks,
-//      redundant-edge skipping), local flatten, local component sizes.
-//   X  cross-band unions over DSMEM, one thread per boundary column.
-//   Z  every local root resolves its global root (read-only chase) and adds
-//      its local size there; other runs resolve through their local root.
-//   K  kept roots (size >= min_points), ordered scan over run ids, cluster
-//      prefix -> label = 1 + rank of the component's first cell among kept
-//      components, which is the reference's first-encounter numbering after
+//   U  band-local union-find over run ids in shared memory: non-redundant
+//      edges listed, every run hooked under its smallest listed neighbour,
+//      then all edges united (path halving); local flatten; run lengths
+//      added to local roots.
+//   X  cross-band unions over DSMEM (boundary edges listed, then united).
+//   Z  every band-local root resolves its global root and adds its size there.
+//   K  kept roots (size >= min_points): kept bits and word prefixes per band,
+//      band bases -> label = 1 + rank of the component's first cell among kept
+//      components, the reference's first-encounter numbering after
 //      _renumber_roots and filter_small (SURVEY.md finding 2).
-//   L  run labels, then per-cell labels with 16-byte streaming stores.
+//   L  run labels from the root's band (DSMEM), then per-cell labels with
+//      16-byte streaming stores.
 //
 // A band with more runs than the node capacity NC marks the frame; the whole
 // cluster then leaves and the frame is appended to the overflow list, which
-// rs_dense_kernel processes right after (stream-ordered).
+// rs_dense_kernel processes right after (a programmatic dependent launch).
 #pragma once
 
 #include "rs_common.cuh"
