@@ -14,6 +14,12 @@
  *                          build_connectivity (connectivity.py:64-92): the
  *                          per-pixel ground mask and edge images, for parity
  *                          checks of the edge decisions on their own.
+ *   rs_project             replaces range_image.project (range_image.py:57-115)
+ *                          for B point clouds at once.
+ *   rs_labels_to_points    replaces range_image.labels_to_points
+ *                          (range_image.py:130-141).  With rs_project and
+ *                          rs_segment_batch this is Pipeline.segment_cloud
+ *                          (pipeline.py:133-158) on the GPU.
  *
  * All entry points return RS_OK (0) or a status code; rs_last_error() gives a
  * message for the calling thread.  Invalid arguments are rejected before any
@@ -102,6 +108,38 @@ int rs_segment_batch_host(const rs_config *cfg, const float *h_tables, const flo
 int rs_stage_masks(const rs_config *cfg, const float *d_tables, const float *d_ranges,
                    int32_t batch, uint8_t *d_ground, uint8_t *d_horizontal,
                    uint8_t *d_vertical, void *stream);
+
+/* ---- point clouds --------------------------------------------------------- */
+
+typedef struct rs_project_config {
+    int32_t height, width;       /* H (channels), W (columns) of the range image */
+    int32_t descending;          /* channel_angles[0] > channel_angles[H-1] */
+    int32_t reserved;
+    double azimuth_step;         /* radians (math.radians(azimuth_step_deg), sensor.py:83) */
+    double gap_lo, gap_hi;       /* (asc[1]-asc[0])/2, (asc[H-1]-asc[H-2])/2 in float64
+                                    (range_image.py:86-87), asc = ascending channel angles */
+} rs_project_config;
+
+/* Point clouds -> range images (range_image.py:57-115).  Clouds are
+ * concatenated: points float64 [n_points][stride] with x, y, z in the first
+ * three columns (stride >= 3), cloud b = rows offsets[b]..offsets[b+1]-1
+ * (int64 [n_clouds+1], device).  d_asc: the channel angles in ascending order,
+ * float64 radians (np.deg2rad of the configured degrees), [H], device.
+ * Outputs (device): ranges float32 [B][H][W] (0 = empty), point_index int64
+ * [B][H][W] (index within the cloud, -1 = empty), counts int64 [B][2] =
+ * (n_dropped, n_overwritten).  The nearest return wins a cell; among equal
+ * float64 ranges the highest point index, as in the reference.  Asynchronous
+ * on `stream`.  Inputs must be finite. */
+int rs_project(const rs_project_config *pc, const double *d_asc, const double *d_points,
+               int32_t stride, const int64_t *d_offsets, int32_t n_clouds, int64_t n_points,
+               float *d_ranges, int64_t *d_point_index, int64_t *d_counts, void *stream);
+
+/* Labels back to points (range_image.py:130-141): point_labels int32
+ * [n_points] (device) gets labels[b][cell] for the point that won the cell,
+ * 0 for dropped and overwritten points. */
+int rs_labels_to_points(const int32_t *d_labels, const int64_t *d_point_index, const int64_t *d_offsets,
+                        int32_t n_clouds, int32_t height, int32_t width, int64_t n_points,
+                        int32_t *d_point_labels, void *stream);
 
 /* Debug: per-CTA phase timestamps (clock64, 16 slots per CTA) of the last
  * launch.  Only a library built with -DRS_PHASE_PROF records them; the

@@ -116,3 +116,46 @@ def segment_batch(ranges, packed, nthreads=None, sizes_stride=None):
     if rc != 0:
         raise MemoryError("oracle allocation failed")
     return labels, ncl, sizes
+
+
+class _ProjCfg(ctypes.Structure):
+    _fields_ = [("height", ctypes.c_int32), ("width", ctypes.c_int32),
+                ("descending", ctypes.c_int32), ("azimuth_step", ctypes.c_double),
+                ("asc", ctypes.POINTER(ctypes.c_double))]
+
+
+def project(points, model):
+    """range_image.project restated in C (project_oracle.c).
+
+    Returns ``(ranges f32 [H,W], point_index i64 [H,W], n_dropped, n_overwritten)``.
+    """
+    pts = np.ascontiguousarray(np.asarray(points, dtype=np.float64))
+    if pts.ndim != 2 or pts.shape[1] < 3 or pts.shape[0] == 0:
+        raise ValueError("expected a nonempty (N, 3) point array")
+    ang = np.asarray(model.channel_angles, dtype=np.float64)
+    desc = bool(ang[0] > ang[-1])
+    asc = np.ascontiguousarray(ang[::-1] if desc else ang)
+    cfg = _ProjCfg(model.height, model.width, int(desc), float(model.azimuth_step),
+                   _ptr(asc, ctypes.c_double))
+    H, W = model.height, model.width
+    ranges = np.zeros((H, W), np.float32)
+    pidx = np.zeros((H, W), np.int64)
+    counts = np.zeros(2, np.int64)
+    rc = lib().oracle_project(_ptr(pts, ctypes.c_double), ctypes.c_int64(pts.shape[0]),
+                              ctypes.c_int32(pts.shape[1]), ctypes.byref(cfg),
+                              _ptr(ranges, ctypes.c_float), _ptr(pidx, ctypes.c_int64),
+                              _ptr(counts, ctypes.c_int64))
+    if rc != 0:
+        raise MemoryError("oracle allocation failed")
+    return ranges, pidx, int(counts[0]), int(counts[1])
+
+
+def labels_to_points(labels, point_index, n_points):
+    """range_image.labels_to_points restated in C."""
+    lab = np.ascontiguousarray(labels, dtype=np.int32)
+    pidx = np.ascontiguousarray(point_index, dtype=np.int64)
+    out = np.zeros(int(n_points), np.int32)
+    lib().oracle_labels_to_points(_ptr(lab, ctypes.c_int32), _ptr(pidx, ctypes.c_int64),
+                                  ctypes.c_int64(pidx.size), ctypes.c_int64(n_points),
+                                  _ptr(out, ctypes.c_int32))
+    return out

@@ -8,6 +8,7 @@ include/rangeseg_b200.h.  Names mirror the reference's public API
 (pkg/src/rangeseg/__init__.py:11-31) for the path.
 """
 
+from .cloud import SegOutput, labels_to_points, project
 from .config import (PRESETS, DistanceThreshold, GroundParams, MCPattern,
                      PipelineConfig, parse_offsets, preset_pattern, skip_pattern)
 from .pipeline import (STAGES, BatchResult, LabelImage, Pipeline, RangeImage,

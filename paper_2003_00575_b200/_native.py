@@ -18,8 +18,8 @@ MAX_OFFSETS = 32
 RS_OK, RS_EINVAL, RS_ECUDA, RS_ETOOLARGE, RS_ENODEV = range(5)
 
 EXPORTS = ("rs_tables_count", "rs_plan", "rs_plan_detail", "rs_workspace_size",
-           "rs_segment_batch", "rs_segment_batch_host", "rs_stage_masks", "rs_phase_profile",
-           "rs_last_error", "rs_version")
+           "rs_segment_batch", "rs_segment_batch_host", "rs_stage_masks", "rs_project",
+           "rs_labels_to_points", "rs_phase_profile", "rs_last_error", "rs_version")
 
 
 class RsConfig(ctypes.Structure):
@@ -32,6 +32,13 @@ class RsConfig(ctypes.Structure):
                 ("keep_above", ctypes.c_float), ("two_cos_h", ctypes.c_float),
                 ("rows_per_cta", ctypes.c_int32),
                 ("reserved", ctypes.c_int32 * 3)]
+
+
+class RsProjectConfig(ctypes.Structure):
+    _fields_ = [("height", ctypes.c_int32), ("width", ctypes.c_int32),
+                ("descending", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("azimuth_step", ctypes.c_double),
+                ("gap_lo", ctypes.c_double), ("gap_hi", ctypes.c_double)]
 
 
 _lib = None
@@ -67,6 +74,12 @@ def lib():
         L.rs_stage_masks.restype = ctypes.c_int
         L.rs_stage_masks.argtypes = [ctypes.POINTER(RsConfig), _P, _P, ctypes.c_int32,
                                      _P, _P, _P, _P]
+        L.rs_project.restype = ctypes.c_int
+        L.rs_project.argtypes = [ctypes.POINTER(RsProjectConfig), _P, _P, ctypes.c_int32, _P,
+                                 ctypes.c_int32, ctypes.c_int64, _P, _P, _P, _P]
+        L.rs_labels_to_points.restype = ctypes.c_int
+        L.rs_labels_to_points.argtypes = [_P, _P, _P, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                          ctypes.c_int64, _P, _P]
         L.rs_phase_profile.restype = ctypes.c_int
         L.rs_phase_profile.argtypes = [_P, ctypes.c_int32]
         L.rs_last_error.restype = ctypes.c_char_p

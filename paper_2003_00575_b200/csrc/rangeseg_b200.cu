@@ -23,6 +23,7 @@
 #include "rs_dense.cuh"
 #include "rs_fast.cuh"
 #include "rs_stage.cuh"
+#include "rs_project.cuh"
 
 using rs::KArgs;
 
@@ -593,6 +594,73 @@ int rs_segment_batch_host(const rs_config *cfg, const float *h_tables, const flo
     return st ? st : sst;
 }
 
+int rs_project(const rs_project_config *pc, const double *d_asc, const double *d_points, int32_t stride,
+               const int64_t *d_offsets, int32_t n_clouds, int64_t n_points, float *d_ranges,
+               int64_t *d_point_index, int64_t *d_counts, void *stream) {
+    if (!pc) return fail(RS_EINVAL, "config is NULL");
+    if (pc->height < 2 || pc->width < 1) return fail(RS_EINVAL, "need at least 2 channels and 1 column");
+    if (!(pc->azimuth_step > 0)) return fail(RS_EINVAL, "azimuth step must be > 0");
+    if (stride < 3) return fail(RS_EINVAL, "points need at least 3 columns");
+    if (n_clouds < 0 || n_points < 0) return fail(RS_EINVAL, "negative sizes");
+    if (n_points >= (1LL << 31)) return fail(RS_ETOOLARGE, "at most 2^31 - 1 points per call");
+    if (n_clouds == 0) return RS_OK;
+    if (!d_asc || !d_offsets || !d_ranges || !d_point_index || !d_counts || (n_points > 0 && !d_points))
+        return fail(RS_EINVAL, "NULL buffer");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int64_t cells = (int64_t)n_clouds * pc->height * pc->width;
+    rs::ProjArgs a{};
+    a.pts = d_points;
+    a.stride = stride;
+    a.offsets = d_offsets;
+    a.B = n_clouds;
+    a.H = pc->height;
+    a.W = pc->width;
+    a.desc = pc->descending ? 1 : 0;
+    a.step = pc->azimuth_step;
+    a.gap_lo = pc->gap_lo;
+    a.gap_hi = pc->gap_hi;
+    a.two_pi = 2.0 * 3.141592653589793;   // 2.0 * np.pi (range_image.py:93)
+    a.asc = d_asc;
+    a.n_total = n_points;
+    a.ranges = d_ranges;
+    a.point_index = d_point_index;
+    a.counts = d_counts;
+    int st;
+    // scratch: +inf-like range bits (all ones) and index -1 (all ones)
+    if ((st = cuda_check(cudaMemsetAsync(d_point_index, 0xff, (size_t)cells * 8, s), "memset point_index")) ||
+        (st = cuda_check(cudaMemsetAsync(d_ranges, 0xff, (size_t)cells * 4, s), "memset ranges")) ||
+        (st = cuda_check(cudaMemsetAsync(d_counts, 0, (size_t)n_clouds * 16, s), "memset counts")))
+        return st;
+    const unsigned tp = rs::kProjThreads;
+    if (n_points > 0) {
+        const unsigned gp = (unsigned)((n_points + tp - 1) / tp);
+        rs::rs_project_min_kernel<<<gp, tp, 0, s>>>(a);
+        rs::rs_project_index_kernel<<<gp, tp, 0, s>>>(a);
+    }
+    rs::rs_project_finish_kernel<<<(unsigned)((cells + tp - 1) / tp), tp, 0, s>>>(a);
+    rs::rs_project_counts_kernel<<<(unsigned)((n_clouds + 127) / 128), 128, 0, s>>>(a);
+    return cuda_check(cudaGetLastError(), "rs_project launch");
+}
+
+int rs_labels_to_points(const int32_t *d_labels, const int64_t *d_point_index, const int64_t *d_offsets,
+                        int32_t n_clouds, int32_t height, int32_t width, int64_t n_points,
+                        int32_t *d_point_labels, void *stream) {
+    if (n_clouds < 0 || n_points < 0 || height < 1 || width < 1) return fail(RS_EINVAL, "bad sizes");
+    if (n_clouds == 0) return RS_OK;
+    if (!d_labels || !d_point_index || !d_offsets || (n_points > 0 && !d_point_labels))
+        return fail(RS_EINVAL, "NULL buffer");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    int st;
+    if (n_points > 0 &&
+        (st = cuda_check(cudaMemsetAsync(d_point_labels, 0, (size_t)n_points * 4, s), "memset point labels")))
+        return st;
+    const int64_t HW = (int64_t)height * width, cells = (int64_t)n_clouds * HW;
+    rs::rs_labels_to_points_kernel<<<(unsigned)((cells + rs::kProjThreads - 1) / rs::kProjThreads),
+                                     rs::kProjThreads, 0, s>>>(d_labels, d_point_index, d_offsets, n_clouds, HW,
+                                                               d_point_labels);
+    return cuda_check(cudaGetLastError(), "rs_labels_to_points launch");
+}
+
 int rs_phase_profile(int64_t *host_out, int32_t max_ctas) {
 #ifdef RS_PHASE_PROF
     const int n = std::min<int>(max_ctas, rs::kProfCtas);
@@ -608,6 +676,6 @@ int rs_phase_profile(int64_t *host_out, int32_t max_ctas) {
 
 const char *rs_last_error(void) { return g_err.c_str(); }
 
-int rs_version(void) { return 200; }
+int rs_version(void) { return 201; }
 
 }  // extern "C"

@@ -1,0 +1,166 @@
+// rs_project.cuh — point clouds <-> range images on the GPU:
+// range_image.project (/root/reference/pkg/src/rangeseg/range_image.py:57-115)
+// and labels_to_points (:130-141), for a batch of clouds concatenated in one
+// float64 array with CSR offsets.
+//
+// Per point, in float64 with the reference's op order (no contraction):
+// range, elevation = asin(clip(z / r)), nearest channel by binary search plus
+// the reference's <= tie rule, the half-gap field-of-view gate, azimuth =
+// atan2(y, x) (+2*pi when negative) and numpy's floor_divide bin.  A cell keeps
+// the smallest range and, among equal ranges, the highest point index (the
+// reference assigns in a stable descending-range order, :98-104):
+//   1. atomicMin of the range's float64 bits per cell (positive doubles order
+//      like their bit patterns),
+//   2. atomicMax of the point index over the points that hit that minimum,
+//   3. per cell: float32 range and int64 index, counts of filled cells.
+// Scratch lives in the outputs themselves (the minimum in the point_index
+// buffer, the index in the ranges buffer) until step 3 rewrites them.
+//
+// asin / atan2 are CUDA's double-precision functions; like numpy's vectorised
+// float64 arcsin (which already differs from the C library's), they may differ
+// in the last ulp, which changes a decision only for a point within ~1e-16
+// relative of a channel midpoint, the field-of-view edge or a column edge
+// (tests/golden.py unstable_cells).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "../../include/rangeseg_b200.h"
+
+namespace rs {
+
+constexpr int kProjThreads = 256;
+
+struct ProjArgs {
+    const double *pts;
+    int32_t stride;
+    const int64_t *offsets;   // [B + 1]
+    int32_t B, H, W, desc;
+    double step, gap_lo, gap_hi, two_pi;
+    const double *asc;        // [H] ascending channel angles (radians)
+    int64_t n_total;
+    float *ranges;            // [B][H][W]; int32 point index scratch until step 3
+    int64_t *point_index;     // [B][H][W]; float64 range bits scratch until step 3
+    int64_t *counts;          // [B][2]
+};
+
+__device__ __forceinline__ int cloud_of(const ProjArgs &a, int64_t i) {
+    int lo = 0, hi = a.B;   // offsets[lo] <= i < offsets[hi]
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (__ldg(a.offsets + mid) <= i) lo = mid; else hi = mid;
+    }
+    return lo;
+}
+
+// numpy float64 floor_divide (npy_divmod's quotient) for a >= 0, b > 0
+__device__ __forceinline__ double py_floor_divide(double x, double y) {
+    const double mod = fmod(x, y);
+    const double div = __ddiv_rn(__dsub_rn(x, mod), y);
+    if (div == 0.0) return copysign(0.0, __ddiv_rn(x, y));
+    double fl = floor(div);
+    if (__dsub_rn(div, fl) > 0.5) fl = __dadd_rn(fl, 1.0);
+    return fl;
+}
+
+// cell (index within the frame) of point i, or -1 when it is dropped; r = its range
+__device__ __forceinline__ int64_t proj_cell(const ProjArgs &a, const double *p, double &r) {
+    const double x = p[0], y = p[1], z = p[2];
+    r = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y)), __dmul_rn(z, z)));
+    if (!(r > 0.0)) return -1;           // the origin, NaN coordinates: dropped (ok = r > 0)
+    double q = __ddiv_rn(z, r);
+    if (isnan(q)) return -1;             // np.clip keeps NaN, asin(NaN) fails the gate
+    q = fmin(fmax(q, -1.0), 1.0);
+    const double el = asin(q);
+    const int H = a.H;
+    int pos = 0, hi = H;            // searchsorted(asc, el, side="left")
+    while (pos < hi) {
+        const int mid = (pos + hi) >> 1;
+        if (__ldg(a.asc + mid) < el) pos = mid + 1; else hi = mid;
+    }
+    const int lo_i = min(max(pos - 1, 0), H - 1), hi_i = min(max(pos, 0), H - 1);
+    const double alo = __ldg(a.asc + lo_i), ahi = __ldg(a.asc + hi_i);
+    const int nearest = fabs(__dsub_rn(el, alo)) <= fabs(__dsub_rn(ahi, el)) ? lo_i : hi_i;
+    const double a0 = __ldg(a.asc), aH = __ldg(a.asc + H - 1);
+    if (!(el >= __dsub_rn(a0, a.gap_lo) && el <= __dadd_rn(aH, a.gap_hi))) return -1;
+    const int row = a.desc ? H - 1 - nearest : nearest;
+    double az = atan2(y, x);
+    if (az < 0.0) az = __dadd_rn(az, a.two_pi);
+    long long c = (long long)py_floor_divide(az, a.step) % a.W;
+    if (c < 0) c += a.W;
+    return (int64_t)row * a.W + c;
+}
+
+__global__ void __launch_bounds__(kProjThreads) rs_project_min_kernel(const __grid_constant__ ProjArgs a) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int b = -1;
+    int64_t cell = -1;
+    if (i < a.n_total) {
+        b = cloud_of(a, i);
+        double r;
+        cell = proj_cell(a, a.pts + i * a.stride, r);
+        if (cell >= 0)
+            atomicMin(reinterpret_cast<unsigned long long *>(a.point_index) + (int64_t)b * a.H * a.W + cell,
+                      (unsigned long long)__double_as_longlong(r));
+    }
+    // points in the field of view, one atomic per (warp, cloud)
+    const unsigned lanes = __match_any_sync(0xffffffffu, b);
+    const unsigned inf = __ballot_sync(0xffffffffu, cell >= 0) & lanes;
+    if (b >= 0 && (threadIdx.x & 31) == __ffs(lanes) - 1 && inf)
+        atomicAdd(reinterpret_cast<unsigned long long *>(a.counts) + 2 * b, (unsigned long long)__popc(inf));
+}
+
+__global__ void __launch_bounds__(kProjThreads) rs_project_index_kernel(const __grid_constant__ ProjArgs a) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= a.n_total) return;
+    const int b = cloud_of(a, i);
+    double r;
+    const int64_t cell = proj_cell(a, a.pts + i * a.stride, r);
+    if (cell < 0) return;
+    const int64_t p = (int64_t)b * a.H * a.W + cell;
+    const unsigned long long m = *reinterpret_cast<const volatile unsigned long long *>(a.point_index + p);
+    if (m == (unsigned long long)__double_as_longlong(r))
+        atomicMax(reinterpret_cast<int *>(a.ranges) + p, (int)(i - __ldg(a.offsets + b)));
+}
+
+__global__ void __launch_bounds__(kProjThreads) rs_project_finish_kernel(const __grid_constant__ ProjArgs a) {
+    const int64_t HW = (int64_t)a.H * a.W;
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int b = -1;
+    bool filled = false;
+    if (p < (int64_t)a.B * HW) {
+        b = (int)(p / HW);
+        const int ix = reinterpret_cast<const int *>(a.ranges)[p];
+        const unsigned long long m = reinterpret_cast<const unsigned long long *>(a.point_index)[p];
+        filled = ix >= 0;
+        a.ranges[p] = filled ? __double2float_rn(__longlong_as_double((long long)m)) : 0.f;
+        a.point_index[p] = filled ? (int64_t)ix : (int64_t)-1;
+    }
+    const unsigned lanes = __match_any_sync(0xffffffffu, b);
+    const unsigned f = __ballot_sync(0xffffffffu, filled) & lanes;
+    if (b >= 0 && (threadIdx.x & 31) == __ffs(lanes) - 1 && f)
+        atomicAdd(reinterpret_cast<unsigned long long *>(a.counts) + 2 * b + 1, (unsigned long long)__popc(f));
+}
+
+// counts[b] = (n_in, n_filled) -> (n_dropped, n_overwritten)
+__global__ void rs_project_counts_kernel(const __grid_constant__ ProjArgs a) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= a.B) return;
+    const int64_t n = __ldg(a.offsets + b + 1) - __ldg(a.offsets + b);
+    const int64_t n_in = a.counts[2 * b], filled = a.counts[2 * b + 1];
+    a.counts[2 * b] = n - n_in;
+    a.counts[2 * b + 1] = n_in - filled;
+}
+
+__global__ void __launch_bounds__(kProjThreads)
+    rs_labels_to_points_kernel(const int32_t *labels, const int64_t *point_index, const int64_t *offsets, int B,
+                               int64_t HW, int32_t *out) {
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= (int64_t)B * HW) return;
+    const int64_t ix = point_index[p];
+    if (ix >= 0) out[__ldg(offsets + p / HW) + ix] = labels[p];
+}
+
+}  // namespace rs

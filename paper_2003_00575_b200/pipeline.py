@@ -48,6 +48,13 @@ class RangeImage:
     def shape(self):
         return self.ranges.shape
 
+    @property
+    def n_projected(self) -> int:
+        """Number of points that won a cell (range_image.py:35-40)."""
+        if self.point_index is None:
+            return int(np.count_nonzero(self.ranges))
+        return int(np.count_nonzero(self.point_index >= 0))
+
     def valid_mask(self) -> np.ndarray:
         return self.ranges > 0
 
@@ -282,6 +289,54 @@ class Pipeline:
         rec.ccl = ev0.elapsed_time(ev1)
         rec.total = (time.perf_counter() - t0) * 1e3
         return li, rec
+
+
+    # -- point clouds (pipeline.py:133-158) -------------------------------------
+    def segment_clouds(self, clouds):
+        """Project, cluster and back-project a list of clouds in one batch:
+        ``[(SegOutput, TimingRecord)]``, each equal to ``segment_cloud``."""
+        from . import cloud
+        rec = TimingRecord()
+        t0 = time.perf_counter()
+        self._require_cuda()
+        arrs = [np.asarray(c) for c in clouds]
+        H, W = self.shape
+        out = [None] * len(arrs)
+        live = [i for i, a in enumerate(arrs) if a.size > 0]
+        for i, a in enumerate(arrs):
+            if a.size == 0:   # the reference's empty-cloud result (pipeline.py:137-143)
+                empty = LabelImage(labels=np.zeros((H, W), np.int32), cluster_sizes=np.array([H * W]))
+                out[i] = (cloud.SegOutput(point_labels=np.zeros(0, np.int32), label_image=empty),
+                          TimingRecord())
+        if live:
+            pts = [cloud._check_points(arrs[i]) for i in live]
+            x = torch.from_numpy(np.concatenate(pts) if len(pts) > 1 else pts[0]).to(self.device)
+            off = torch.from_numpy(np.cumsum([0] + [p.shape[0] for p in pts]).astype(np.int64)).to(self.device)
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+            ev[0].record()
+            ranges, pidx, _ = cloud.project_batch(x, off, self.model)
+            ev[1].record()
+            res = self.segment_batch(ranges)
+            ev[2].record()
+            plab = cloud.labels_to_points_batch(res.labels, pidx, off)
+            ev[3].record()
+            plab = plab.cpu().numpy()
+            labels = res.labels.cpu().numpy()
+            ncl = res.n_clusters.cpu().numpy()
+            sizes = res.cluster_sizes.cpu().numpy()
+            offs = off.cpu().numpy()
+            rec.project = ev[0].elapsed_time(ev[1]) + ev[2].elapsed_time(ev[3])
+            rec.ccl = ev[1].elapsed_time(ev[2])
+            for j, i in enumerate(live):
+                li = LabelImage(labels=labels[j], cluster_sizes=sizes[j, :int(ncl[j]) + 1].copy())
+                out[i] = (cloud.SegOutput(point_labels=plab[offs[j]:offs[j + 1]], label_image=li), rec)
+        rec.total = (time.perf_counter() - t0) * 1e3
+        return out
+
+    def segment_cloud(self, points):
+        """Project a cloud, cluster it and carry labels back to the points
+        (pipeline.py:133-158): ``(SegOutput, TimingRecord)``."""
+        return self.segment_clouds([points])[0]
 
 
 def segment_in_parallel(range_images, model: SensorModel,

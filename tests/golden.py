@@ -70,3 +70,53 @@ def case(group, case_key, frame_key=None):
                   unpack(st, f"{case_key}/horizontal", (H, W)),
                   unpack(st, f"{case_key}/vertical", (H - 1, W)))
     return m, cfg, ranges, st[f"{case_key}/labels"], st[f"{case_key}/sizes"], stages
+
+
+# ---------------------------------------------------------------- project ----
+def project_cases():
+    return sorted({k.rsplit("/", 1)[0] for k in load("project")})
+
+
+def project_case(key):
+    st = load("project")
+    m = SensorModel(st[f"{key}/angles_deg"], float(st[f"{key}/step_deg"]), float(st[f"{key}/mount"]),
+                    width=int(st[f"{key}/width"]))
+    return m, {k.rsplit("/", 1)[1]: v for k, v in st.items() if k.rsplit("/", 1)[0] == key}
+
+
+def unstable_cells(points, model, rel=1e-12):
+    """Cells a point may land in when its elevation sits within ``rel`` of a
+    channel midpoint / field-of-view edge, or its azimuth within ``rel`` of a
+    column edge.  There the decision turns on the last ulp of asin / atan2,
+    which differ between libraries (numpy's vectorised float64 arcsin is not the
+    C library's; CUDA's is a third).  Returns a bool [H, W] mask and the number
+    of such points.  Everywhere else projection results must be bit-identical.
+    """
+    H, W = model.height, model.width
+    p = np.asarray(points, dtype=np.float64)[:, :3]
+    r = np.sqrt((p[:, 0] * p[:, 0] + p[:, 1] * p[:, 1]) + p[:, 2] * p[:, 2])
+    ok = r > 0
+    el = np.arcsin(np.clip(np.divide(p[:, 2], r, where=ok, out=np.zeros_like(r)), -1, 1))
+    ang = np.asarray(model.channel_angles, dtype=np.float64)
+    desc = ang[0] > ang[-1]
+    asc = ang[::-1] if desc else ang
+    bounds = np.concatenate([(asc[1:] + asc[:-1]) / 2, [asc[0] - (asc[1] - asc[0]) / 2,
+                                                       asc[-1] + (asc[-1] - asc[-2]) / 2]])
+    near_el = (np.abs(el[:, None] - bounds[None, :]) <= rel * np.maximum(1.0, np.abs(bounds))).any(1)
+    az = np.arctan2(p[:, 1], p[:, 0])
+    az = np.where(az < 0, az + 2 * np.pi, az)
+    q = az / model.azimuth_step
+    near_az = (np.abs(q - np.round(q)) <= rel * np.maximum(1.0, np.abs(q))) | \
+              (np.abs(az - 2 * np.pi) <= rel) | (np.abs(az) <= rel)
+    amb = ok & (near_el | near_az)
+    mask = np.zeros((H, W), bool)
+    for i in np.flatnonzero(amb):
+        row = int(np.argmin(np.abs(asc - el[i])))
+        row = H - 1 - row if desc else row
+        col = int(np.floor(q[i])) % W
+        for dr in (-1, 0, 1):
+            for dc in (-1, 0, 1):
+                rr = row + dr
+                if 0 <= rr < H:
+                    mask[rr, (col + dc) % W] = True
+    return mask, int(amb.sum())

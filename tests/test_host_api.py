@@ -131,7 +131,7 @@ def test_library_exports_every_header_symbol():
     assert declared == set(_native.EXPORTS)
     for name in declared:
         assert hasattr(lib, name), name
-    assert lib.rs_version() == 200
+    assert lib.rs_version() == 201
 
 
 def test_tables_count_matches_layout():

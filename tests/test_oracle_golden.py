@@ -45,3 +45,29 @@ def test_oracle_batch_equals_per_frame():
         assert np.array_equal(lab[b], l1)
         assert ncl[b] == len(s1) - 1
         assert np.array_equal(sz[b, :len(s1)], s1)
+
+
+# ------------------------------------------------- point clouds (§8(f)1) -----
+@pytest.mark.parametrize("key", golden.project_cases())
+def test_oracle_project_matches_reference(key):
+    """project_oracle.c against range_image.project's recorded outputs:
+    bit-identical on every cell no boundary-ambiguous point can reach (the
+    oracle's asin is the C library's, the reference ran numpy's vectorised
+    arcsin; they differ in the last ulp)."""
+    m, c = golden.project_case(key)
+    ranges, pidx, n_dropped, n_over = oracle.project(c["points"], m)
+    unstable, n_amb = golden.unstable_cells(c["points"], m)
+    st = ~unstable
+    assert np.array_equal(ranges[st].view(np.uint32), c["ranges"][st].view(np.uint32))
+    assert np.array_equal(pidx[st], c["point_index"][st])
+    assert abs(n_dropped - c["counts"][1]) <= n_amb
+    assert abs(n_over - c["counts"][2]) <= 2 * n_amb
+    if n_amb == 0:
+        assert (n_dropped, n_over) == (c["counts"][1], c["counts"][2])
+
+
+@pytest.mark.parametrize("key", golden.project_cases())
+def test_oracle_labels_to_points_matches_reference(key):
+    m, c = golden.project_case(key)
+    got = oracle.labels_to_points(c["labels"], c["point_index"], c["counts"][0])
+    assert np.array_equal(got, c["point_labels"])
