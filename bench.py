@@ -54,6 +54,7 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=10.0)
+    p.add_argument("--no-cloud", action="store_true", help="skip the point-cloud path measurement")
     return p.parse_args()
 
 
@@ -182,6 +183,74 @@ def cpu_sample(frames_np, packed, seconds, nthreads=1):
         el = time.perf_counter() - t0
         if el >= seconds:
             return done, el
+
+
+def cloud_bench(args, pipe, frames, spec, flush):
+    """Point-cloud path (Pipeline.segment_cloud on B clouds):
+    the config's frames back-projected to float64 points (one point per valid
+    cell, cell-centre azimuth), resident in HBM; per step rs_project ->
+    rs_segment_batch -> rs_labels_to_points, device-timed.  CPU: the oracle's
+    project + segment + labels_to_points on two clouds, one thread."""
+    import numpy as np
+    import torch
+    from paper_2003_00575_b200 import cloud
+    dev = frames.device
+    model = pipe.model
+    r = frames.double()
+    el = torch.as_tensor(np.asarray(model.channel_angles), dtype=torch.float64, device=dev)[:, None]
+    az = (torch.arange(model.width, dtype=torch.float64, device=dev) + 0.5) * model.azimuth_step
+    keep = r > 0
+    xyz = torch.stack([r * torch.cos(el) * torch.cos(az), r * torch.cos(el) * torch.sin(az),
+                       r * torch.sin(el).expand_as(r)], -1)
+    pts = xyz[keep].contiguous()
+    off = torch.zeros(frames.shape[0] + 1, dtype=torch.int64, device=dev)
+    off[1:] = torch.cumsum(keep.flatten(1).sum(1), 0)
+    n = int(off[-1].item())
+
+    def step():
+        ranges, pidx, _ = cloud.project_batch(pts, off, model)
+        res = pipe.segment_batch(ranges)
+        return cloud.labels_to_points_batch(res.labels, pidx, off)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    steps = max(5, args.steps // 10)
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(steps)]
+    for e in ev:
+        flush.zero_()
+        e[0].record()
+        ranges, pidx, _ = cloud.project_batch(pts, off, model)
+        e[1].record()
+        res = pipe.segment_batch(ranges)
+        e[2].record()
+        cloud.labels_to_points_batch(res.labels, pidx, off)
+        e[3].record()
+    torch.cuda.synchronize()
+    tot = sum(e[0].elapsed_time(e[3]) for e in ev) / steps
+    proj = sum(e[0].elapsed_time(e[1]) for e in ev) / steps
+    seg = sum(e[1].elapsed_time(e[2]) for e in ev) / steps
+    back = sum(e[2].elapsed_time(e[3]) for e in ev) / steps
+    B = frames.shape[0]
+    out = {"value": B / (tot * 1e-3), "unit": "clouds/s", "points_per_s": n / (tot * 1e-3),
+           "points_per_cloud": n / B, "ms_per_step": tot, "steps": steps,
+           "stages_ms": {"project": proj, "segment": seg, "labels_to_points": back},
+           "path": "cloud.project_batch -> Pipeline.segment_batch -> cloud.labels_to_points_batch "
+                   "(rs_project, rs_segment_batch, rs_labels_to_points), float64 points in HBM"}
+    if not args.no_cpu_baseline:
+        from oracle import oracle
+        offs = off.cpu().numpy()
+        host = pts[: int(offs[2])].cpu().numpy()
+        t0 = time.perf_counter()
+        for b in range(2):
+            c = host[offs[b]:offs[b + 1]]
+            wr, wp, _, _ = oracle.project(c, model)
+            wl, _ = oracle.segment_frame(wr, pipe.packed)
+            oracle.labels_to_points(wl, wp, len(c))
+        el_s = time.perf_counter() - t0
+        out["cpu_baseline"] = {"value": 2 / el_s, "unit": "clouds/s", "cores": 1, "kind": "port",
+                               "sample": "2 clouds, oracle project + segment_frame + labels_to_points"}
+    return out
 
 
 def run_reference(args):
@@ -323,6 +392,10 @@ def run_b200(args):
             dist.destroy_process_group()
         return
 
+    cloud_path = None
+    if not args.no_cloud and world == 1:
+        cloud_path = cloud_bench(args, pipe, frames, spec, flush)
+
     cpu = None
     if not args.no_cpu_baseline:
         done, el = cpu_sample(frames.cpu().numpy(), pipe.packed, args.cpu_seconds, 1)
@@ -356,6 +429,7 @@ def run_b200(args):
                      "kernel_ms": ms},
         "cpu_baseline": cpu,
         "e2e": e2e,
+        "cloud_path": cloud_path,
         "gpu_launches": args.steps * (2 if pipe.plan["may_overflow"] else 1),
         "clocks": clk.summary(),
         "wall_s_timed_region": wall,

@@ -129,10 +129,16 @@ typedef struct rs_project_config {
  * [B][H][W] (index within the cloud, -1 = empty), counts int64 [B][2] =
  * (n_dropped, n_overwritten).  The nearest return wins a cell; among equal
  * float64 ranges the highest point index, as in the reference.  Asynchronous
- * on `stream`.  Inputs must be finite. */
+ * on `stream`.  Inputs must be finite.  d_workspace: device scratch of at
+ * least rs_project_workspace_size(n_points) bytes (no initialisation needed). */
 int rs_project(const rs_project_config *pc, const double *d_asc, const double *d_points,
                int32_t stride, const int64_t *d_offsets, int32_t n_clouds, int64_t n_points,
-               float *d_ranges, int64_t *d_point_index, int64_t *d_counts, void *stream);
+               float *d_ranges, int64_t *d_point_index, int64_t *d_counts,
+               void *d_workspace, size_t workspace_size, void *stream);
+
+/* Scratch rs_project needs for n_points points (float64 range bits and an
+ * int32 cell per point; 8-byte aligned). */
+size_t rs_project_workspace_size(int64_t n_points);
 
 /* Labels back to points (range_image.py:130-141): point_labels int32
  * [n_points] (device) gets labels[b][cell] for the point that won the cell,

@@ -67,10 +67,12 @@ def project_batch(points: torch.Tensor, offsets: torch.Tensor, model: SensorMode
     ranges = torch.empty((B, H, W), dtype=torch.float32, device=dev)
     pidx = torch.empty((B, H, W), dtype=torch.int64, device=dev)
     counts = torch.empty((B, 2), dtype=torch.int64, device=dev)
+    wsb = int(_native.lib().rs_project_workspace_size(points.shape[0]))
+    ws = torch.empty((max(wsb, 4),), dtype=torch.uint8, device=dev)
     s = stream if stream is not None else torch.cuda.current_stream(dev)
     st = _native.lib().rs_project(ctypes.byref(pc), _ptr(d_asc), _ptr(points), points.shape[1],
                                   _ptr(offsets), B, points.shape[0], _ptr(ranges), _ptr(pidx),
-                                  _ptr(counts), ctypes.c_void_p(s.cuda_stream))
+                                  _ptr(counts), _ptr(ws), wsb, ctypes.c_void_p(s.cuda_stream))
     _native.check(st, "rs_project")
     return ranges, pidx, counts
 

@@ -596,8 +596,11 @@ int rs_segment_batch_host(const rs_config *cfg, const float *h_tables, const flo
 
 int rs_project(const rs_project_config *pc, const double *d_asc, const double *d_points, int32_t stride,
                const int64_t *d_offsets, int32_t n_clouds, int64_t n_points, float *d_ranges,
-               int64_t *d_point_index, int64_t *d_counts, void *stream) {
+               int64_t *d_point_index, int64_t *d_counts, void *d_workspace, size_t workspace_size,
+               void *stream) {
     if (!pc) return fail(RS_EINVAL, "config is NULL");
+    if (workspace_size < rs_project_workspace_size(n_points) || (n_points > 0 && !d_workspace))
+        return fail(RS_EINVAL, "workspace smaller than rs_project_workspace_size(n_points)");
     if (pc->height < 2 || pc->width < 1) return fail(RS_EINVAL, "need at least 2 channels and 1 column");
     if (!(pc->azimuth_step > 0)) return fail(RS_EINVAL, "azimuth step must be > 0");
     if (stride < 3) return fail(RS_EINVAL, "points need at least 3 columns");
@@ -625,6 +628,8 @@ int rs_project(const rs_project_config *pc, const double *d_asc, const double *d
     a.ranges = d_ranges;
     a.point_index = d_point_index;
     a.counts = d_counts;
+    a.rbits = static_cast<unsigned long long *>(d_workspace);
+    a.cell = reinterpret_cast<int32_t *>(a.rbits + n_points);
     int st;
     // scratch: +inf-like range bits (all ones) and index -1 (all ones)
     if ((st = cuda_check(cudaMemsetAsync(d_point_index, 0xff, (size_t)cells * 8, s), "memset point_index")) ||
@@ -641,6 +646,8 @@ int rs_project(const rs_project_config *pc, const double *d_asc, const double *d
     rs::rs_project_counts_kernel<<<(unsigned)((n_clouds + 127) / 128), 128, 0, s>>>(a);
     return cuda_check(cudaGetLastError(), "rs_project launch");
 }
+
+size_t rs_project_workspace_size(int64_t n_points) { return (size_t)std::max<int64_t>(n_points, 0) * 12u; }
 
 int rs_labels_to_points(const int32_t *d_labels, const int64_t *d_point_index, const int64_t *d_offsets,
                         int32_t n_clouds, int32_t height, int32_t width, int64_t n_points,

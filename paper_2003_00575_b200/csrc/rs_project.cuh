@@ -44,7 +44,33 @@ struct ProjArgs {
     float *ranges;            // [B][H][W]; int32 point index scratch until step 3
     int64_t *point_index;     // [B][H][W]; float64 range bits scratch until step 3
     int64_t *counts;          // [B][2]
+    int32_t *cell;            // [n_total] workspace: cell of each point from step 1, -1 = dropped
+    unsigned long long *rbits;   // [n_total] workspace: float64 range bits of each point
 };
+
+// Adds `v` (per thread) to counts[2*b + slot], with one global atomic per
+// block when the whole block works on one cloud (the usual case), else per
+// (warp, cloud).  Every thread of the block must call it.
+__device__ __forceinline__ void count_add(int64_t *counts, int b, int slot, unsigned v) {
+    __shared__ int sb_first, sb_last;
+    __shared__ unsigned long long s_sum;
+    if (threadIdx.x == 0) { sb_first = b; s_sum = 0; }
+    if (threadIdx.x == blockDim.x - 1) sb_last = b;
+    __syncthreads();
+    const bool uniform = sb_first == sb_last && sb_first >= 0;
+    if (uniform) {
+        unsigned w = __reduce_add_sync(0xffffffffu, v);
+        if ((threadIdx.x & 31) == 0 && w) atomicAdd(&s_sum, (unsigned long long)w);
+        __syncthreads();
+        if (threadIdx.x == 0 && s_sum) atomicAdd(reinterpret_cast<unsigned long long *>(counts) + 2 * b + slot, s_sum);
+    } else {
+        const unsigned lanes = __match_any_sync(0xffffffffu, b);
+        unsigned tot = 0;
+        for (unsigned m = lanes; m; m &= m - 1) tot += __shfl_sync(0xffffffffu, v, __ffs(m) - 1);
+        if (b >= 0 && (threadIdx.x & 31) == __ffs(lanes) - 1 && tot)
+            atomicAdd(reinterpret_cast<unsigned long long *>(counts) + 2 * b + slot, (unsigned long long)tot);
+    }
+}
 
 __device__ __forceinline__ int cloud_of(const ProjArgs &a, int64_t i) {
     int lo = 0, hi = a.B;   // offsets[lo] <= i < offsets[hi]
@@ -101,28 +127,25 @@ __global__ void __launch_bounds__(kProjThreads) rs_project_min_kernel(const __gr
         b = cloud_of(a, i);
         double r;
         cell = proj_cell(a, a.pts + i * a.stride, r);
+        a.cell[i] = (int32_t)cell;
+        a.rbits[i] = (unsigned long long)__double_as_longlong(r);
         if (cell >= 0)
             atomicMin(reinterpret_cast<unsigned long long *>(a.point_index) + (int64_t)b * a.H * a.W + cell,
                       (unsigned long long)__double_as_longlong(r));
     }
-    // points in the field of view, one atomic per (warp, cloud)
-    const unsigned lanes = __match_any_sync(0xffffffffu, b);
-    const unsigned inf = __ballot_sync(0xffffffffu, cell >= 0) & lanes;
-    if (b >= 0 && (threadIdx.x & 31) == __ffs(lanes) - 1 && inf)
-        atomicAdd(reinterpret_cast<unsigned long long *>(a.counts) + 2 * b, (unsigned long long)__popc(inf));
+    count_add(a.counts, b, 0, cell >= 0 ? 1u : 0u);   // points in the field of view
 }
 
 __global__ void __launch_bounds__(kProjThreads) rs_project_index_kernel(const __grid_constant__ ProjArgs a) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= a.n_total) return;
-    const int b = cloud_of(a, i);
-    double r;
-    const int64_t cell = proj_cell(a, a.pts + i * a.stride, r);
+    const int32_t cell = a.cell[i];
     if (cell < 0) return;
-    const int64_t p = (int64_t)b * a.H * a.W + cell;
-    const unsigned long long m = *reinterpret_cast<const volatile unsigned long long *>(a.point_index + p);
-    if (m == (unsigned long long)__double_as_longlong(r))
-        atomicMax(reinterpret_cast<int *>(a.ranges) + p, (int)(i - __ldg(a.offsets + b)));
+    const int b = cloud_of(a, i);
+    const int64_t q = (int64_t)b * a.H * a.W + cell;
+    const unsigned long long m = reinterpret_cast<const unsigned long long *>(a.point_index)[q];
+    if (m == a.rbits[i])
+        atomicMax(reinterpret_cast<int *>(a.ranges) + q, (int)(i - __ldg(a.offsets + b)));
 }
 
 __global__ void __launch_bounds__(kProjThreads) rs_project_finish_kernel(const __grid_constant__ ProjArgs a) {
@@ -138,10 +161,7 @@ __global__ void __launch_bounds__(kProjThreads) rs_project_finish_kernel(const _
         a.ranges[p] = filled ? __double2float_rn(__longlong_as_double((long long)m)) : 0.f;
         a.point_index[p] = filled ? (int64_t)ix : (int64_t)-1;
     }
-    const unsigned lanes = __match_any_sync(0xffffffffu, b);
-    const unsigned f = __ballot_sync(0xffffffffu, filled) & lanes;
-    if (b >= 0 && (threadIdx.x & 31) == __ffs(lanes) - 1 && f)
-        atomicAdd(reinterpret_cast<unsigned long long *>(a.counts) + 2 * b + 1, (unsigned long long)__popc(f));
+    count_add(a.counts, b, 1, filled ? 1u : 0u);
 }
 
 // counts[b] = (n_in, n_filled) -> (n_dropped, n_overwritten)
