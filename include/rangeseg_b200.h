@@ -16,6 +16,8 @@
  *                          checks of the edge decisions on their own.
  *   rs_project             replaces range_image.project (range_image.py:57-115)
  *                          for B point clouds at once.
+ *   rs_contingency         the counting step of evaluation.match_instances
+ *                          (evaluation.py:65-129) for B frames (§8(f)3).
  *   rs_labels_to_points    replaces range_image.labels_to_points
  *                          (range_image.py:130-141).  With rs_project and
  *                          rs_segment_batch this is Pipeline.segment_cloud
@@ -146,6 +148,23 @@ size_t rs_project_workspace_size(int64_t n_points);
 int rs_labels_to_points(const int32_t *d_labels, const int64_t *d_point_index, const int64_t *d_offsets,
                         int32_t n_clouds, int32_t height, int32_t width, int64_t n_points,
                         int32_t *d_point_labels, void *stream);
+
+/* ---- instance scoring (evaluation.py:65-129) ------------ */
+
+/* The (ground-truth instance, predicted cluster) contingency table of B
+ * frames, the counting step of evaluation.match_instances.  gt / pred: int32
+ * per point (0 = none / background, values < 2^22), frames concatenated with
+ * int64 CSR offsets [B+1] (B < 2^19), all device.  Output: d_pairs /
+ * d_counts (int64, capacity n_points) hold the sorted unique keys
+ * (frame << 44 | gt << 22 | pred) over points with gt > 0 or pred > 0 and their
+ * point counts; a last key 0x7fffffffffffffff (if present) counts the points
+ * with gt == pred == 0 and is not a pair.  d_status int64 [2] = (number of
+ * keys, 1 if a label was out of range).  Sizes of instances and clusters are
+ * the row / column sums.  Asynchronous on `stream`. */
+size_t rs_contingency_workspace_size(int64_t n_points);
+int rs_contingency(const int32_t *d_gt, const int32_t *d_pred, const int64_t *d_offsets, int32_t n_frames,
+                   int64_t n_points, int64_t *d_pairs, int64_t *d_counts, int64_t *d_status,
+                   void *d_workspace, size_t workspace_size, void *stream);
 
 /* Debug: per-CTA phase timestamps (clock64, 16 slots per CTA) of the last
  * launch.  Only a library built with -DRS_PHASE_PROF records them; the

@@ -9,6 +9,8 @@ include/rangeseg_b200.h.  Names mirror the reference's public API
 """
 
 from .cloud import SegOutput, labels_to_points, project
+from .evaluation import (EvalConfig, EvalReport, InstanceMatch, instance_iou,
+                         match_instances, precision_at, report_as_dict, summarize)
 from .config import (PRESETS, DistanceThreshold, GroundParams, MCPattern,
                      PipelineConfig, parse_offsets, preset_pattern, skip_pattern)
 from .pipeline import (STAGES, BatchResult, LabelImage, Pipeline, RangeImage,

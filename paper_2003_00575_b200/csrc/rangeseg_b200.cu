@@ -24,6 +24,10 @@
 #include "rs_fast.cuh"
 #include "rs_stage.cuh"
 #include "rs_project.cuh"
+#include "rs_eval.cuh"
+
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_run_length_encode.cuh>
 
 using rs::KArgs;
 
@@ -666,6 +670,62 @@ int rs_labels_to_points(const int32_t *d_labels, const int64_t *d_point_index, c
                                      rs::kProjThreads, 0, s>>>(d_labels, d_point_index, d_offsets, n_clouds, HW,
                                                                d_point_labels);
     return cuda_check(cudaGetLastError(), "rs_labels_to_points launch");
+}
+
+// workspace of rs_contingency: keys in, keys sorted, the invalid-label flag,
+// then CUB's temporary storage (256-byte aligned pieces)
+namespace {
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+size_t cub_temp_bytes(int n) {
+    size_t a = 0, b = 0;
+    cub::DeviceRadixSort::SortKeys(nullptr, a, (const long long *)nullptr, (long long *)nullptr, n);
+    cub::DeviceRunLengthEncode::Encode(nullptr, b, (const long long *)nullptr, (long long *)nullptr,
+                                       (long long *)nullptr, (long long *)nullptr, n);
+    return std::max(a, b);
+}
+}  // namespace
+
+size_t rs_contingency_workspace_size(int64_t n_points) {
+    if (n_points < 0 || n_points >= (1LL << 31)) return 0;
+    const int n = (int)n_points;
+    return 2 * align256((size_t)n * 8) + 256 + align256(cub_temp_bytes(std::max(n, 1)));
+}
+
+int rs_contingency(const int32_t *d_gt, const int32_t *d_pred, const int64_t *d_offsets, int32_t n_frames,
+                   int64_t n_points, int64_t *d_pairs, int64_t *d_counts, int64_t *d_status, void *d_workspace,
+                   size_t workspace_size, void *stream) {
+    if (n_frames < 0 || n_points < 0) return fail(RS_EINVAL, "negative sizes");
+    if (n_frames >= (1 << rs::kEvalFrameBits)) return fail(RS_ETOOLARGE, "at most 2^19 - 1 frames per call");
+    if (n_points >= (1LL << 31)) return fail(RS_ETOOLARGE, "at most 2^31 - 1 points per call");
+    if (workspace_size < rs_contingency_workspace_size(n_points))
+        return fail(RS_EINVAL, "workspace smaller than rs_contingency_workspace_size(n_points)");
+    if (!d_status || (n_points > 0 && (!d_gt || !d_pred || !d_offsets || !d_pairs || !d_counts || !d_workspace)))
+        return fail(RS_EINVAL, "NULL buffer");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    int st;
+    if ((st = cuda_check(cudaMemsetAsync(d_status, 0, 2 * sizeof(int64_t), s), "memset status"))) return st;
+    if (n_points == 0 || n_frames == 0) return RS_OK;
+    const int n = (int)n_points;
+    char *w = static_cast<char *>(d_workspace);
+    long long *keys = reinterpret_cast<long long *>(w);
+    long long *sorted = reinterpret_cast<long long *>(w + align256((size_t)n * 8));
+    int *bad = reinterpret_cast<int *>(w + 2 * align256((size_t)n * 8));
+    void *temp = w + 2 * align256((size_t)n * 8) + 256;
+    size_t temp_bytes = cub_temp_bytes(n);
+    if ((st = cuda_check(cudaMemsetAsync(bad, 0, sizeof(int), s), "memset flag"))) return st;
+    rs::rs_contingency_keys_kernel<<<(unsigned)((n + rs::kEvalThreads - 1) / rs::kEvalThreads), rs::kEvalThreads, 0,
+                                     s>>>(d_gt, d_pred, d_offsets, n_frames, n_points, keys, bad);
+    if ((st = cuda_check(cudaGetLastError(), "contingency keys")) ||
+        (st = cuda_check(cub::DeviceRadixSort::SortKeys(temp, temp_bytes, keys, sorted, n, 0, 64, s),
+                         "radix sort")) ||
+        (st = cuda_check(cub::DeviceRunLengthEncode::Encode(temp, temp_bytes, sorted,
+                                                            reinterpret_cast<long long *>(d_pairs),
+                                                            reinterpret_cast<long long *>(d_counts),
+                                                            reinterpret_cast<long long *>(d_status), n, s),
+                         "run-length encode")) ||
+        (st = cuda_check(cudaMemcpyAsync(d_status + 1, bad, sizeof(int), cudaMemcpyDeviceToDevice, s), "flag")))
+        return st;
+    return RS_OK;
 }
 
 int rs_phase_profile(int64_t *host_out, int32_t max_ctas) {

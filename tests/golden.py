@@ -120,3 +120,15 @@ def unstable_cells(points, model, rel=1e-12):
                 if 0 <= rr < H:
                     mask[rr, (col + dc) % W] = True
     return mask, int(amb.sum())
+
+
+# ------------------------------------------------------------------- eval ----
+def eval_cases():
+    return sorted({k.split("/")[0] for k in load("eval")})
+
+
+def eval_case(key):
+    st = load("eval")
+    matches = [tuple(m) for m in json.loads(str(st[f"{key}/matches"][0]))]
+    summary = json.loads(str(st[f"{key}/summary"][0]))
+    return st[f"{key}/gt"], st[f"{key}/pred"], int(st[f"{key}/min_gt_points"]), matches, summary
