@@ -141,3 +141,32 @@ def test_reference_projection_rules(cuda):
         rs.labels_to_points(np.ones((4, 8), np.int32), rs.from_ranges(np.ones((4, 8), np.float32)))
     seg, _ = rs.Pipeline(m, rs.PipelineConfig(), device="cuda:0").segment_cloud(np.empty((0, 3)))
     assert seg.point_labels.size == 0 and seg.label_image.cluster_sizes[0] == m.height * m.width
+
+
+def test_scan_files_batch_end_to_end(rng, tmp_path, cuda):
+    """KITTI .bin scans -> one pinned upload (io_formats.load_scans_pinned) ->
+    project / segment / labels_to_points on the device -> .label files, equal
+    to per-scan segment_cloud and to the oracle composition."""
+    from paper_2003_00575_b200 import io_formats as io
+    model = rs.default_model()
+    pipe = rs.Pipeline(model, rs.PipelineConfig(min_cluster_points=10), device="cuda:0")
+    paths = []
+    for k in range(4):
+        pts = rng.uniform(-35, 35, size=(int(rng.integers(5000, 30000)), 3)).astype(np.float32)
+        io.write_velodyne_bin(tmp_path / f"{k:06d}.bin", pts, rng.uniform(0, 1, len(pts)))
+        paths.append(tmp_path / f"{k:06d}.bin")
+    x, off = io.load_scans_pinned(paths)
+    ranges, pidx, _ = cloud.project_batch(x, off, model)
+    res = pipe.segment_batch(ranges)
+    plab = cloud.labels_to_points_batch(res.labels, pidx, off).cpu().numpy()
+    offs = off.cpu().numpy()
+    for k, p in enumerate(paths):
+        pts = io.read_velodyne_bin(p)
+        mine = plab[offs[k]:offs[k + 1]]
+        seg, _ = pipe.segment_cloud(pts)
+        assert np.array_equal(mine, seg.point_labels)
+        wr, wp, _, _ = oracle.project(pts, model)
+        wl, _ = oracle.segment_frame(wr, pipe.packed)
+        assert np.array_equal(mine, oracle.labels_to_points(wl, wp, len(pts)))
+        io.write_instance_labels(tmp_path / f"{k:06d}.label", mine)
+        assert np.array_equal(io.read_instance_labels(tmp_path / f"{k:06d}.label", len(pts)), mine)
