@@ -111,6 +111,22 @@ int rs_stage_masks(const rs_config *cfg, const float *d_tables, const float *d_r
                    int32_t batch, uint8_t *d_ground, uint8_t *d_horizontal,
                    uint8_t *d_vertical, void *stream);
 
+/* The stages on their own, with the reference's inputs (device buffers, B
+ * frames, asynchronous on `stream`):
+ * rs_height_image  height_image (range_image.py:118-127): float32 [B][H][W],
+ *                  NaN where there is no return.
+ * rs_ground_mask   extract_ground (ground.py:95-141) given the height image
+ *                  (cfg->ground_removal = 0: the no-return mask only):
+ *                  uint8 [B][H][W], 1 = ground or no return.
+ * rs_connectivity  build_connectivity (connectivity.py:64-92) given a ground
+ *                  mask: horizontal uint8 [B][H][W], vertical [B][H-1][W]. */
+int rs_height_image(const rs_config *cfg, const float *d_tables, const float *d_ranges, int32_t batch,
+                    float *d_height, void *stream);
+int rs_ground_mask(const rs_config *cfg, const float *d_tables, const float *d_ranges, const float *d_height,
+                   int32_t batch, uint8_t *d_mask, void *stream);
+int rs_connectivity(const rs_config *cfg, const float *d_tables, const float *d_ranges, const uint8_t *d_mask,
+                    int32_t batch, uint8_t *d_horizontal, uint8_t *d_vertical, void *stream);
+
 /* ---- point clouds --------------------------------------------------------- */
 
 typedef struct rs_project_config {

@@ -17,6 +17,7 @@ from .pipeline import (STAGES, BatchResult, LabelImage, Pipeline, RangeImage,
                        TimingRecord, from_ranges, segment_in_parallel)
 from .sensor import (SensorConfigError, SensorModel, canonical_offset,
                      default_model, fov_model, load_sensor_model, uniform_model)
+from .stages import ConnectivityImages, GroundMask, build_connectivity, extract_ground, height_image
 from .tables import PackedTables, pack_tables
 
 __version__ = "0.1.0"

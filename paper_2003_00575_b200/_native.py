@@ -20,6 +20,7 @@ RS_OK, RS_EINVAL, RS_ECUDA, RS_ETOOLARGE, RS_ENODEV = range(5)
 EXPORTS = ("rs_tables_count", "rs_plan", "rs_plan_detail", "rs_workspace_size",
            "rs_segment_batch", "rs_segment_batch_host", "rs_stage_masks", "rs_project",
            "rs_project_workspace_size", "rs_contingency", "rs_contingency_workspace_size",
+           "rs_height_image", "rs_ground_mask", "rs_connectivity",
            "rs_labels_to_points", "rs_phase_profile", "rs_last_error", "rs_version")
 
 
@@ -88,6 +89,12 @@ def lib():
         L.rs_contingency.restype = ctypes.c_int
         L.rs_contingency.argtypes = [_P, _P, _P, ctypes.c_int32, ctypes.c_int64, _P, _P, _P, _P,
                                      ctypes.c_size_t, _P]
+        L.rs_height_image.restype = ctypes.c_int
+        L.rs_height_image.argtypes = [ctypes.POINTER(RsConfig), _P, _P, ctypes.c_int32, _P, _P]
+        L.rs_ground_mask.restype = ctypes.c_int
+        L.rs_ground_mask.argtypes = [ctypes.POINTER(RsConfig), _P, _P, _P, ctypes.c_int32, _P, _P]
+        L.rs_connectivity.restype = ctypes.c_int
+        L.rs_connectivity.argtypes = [ctypes.POINTER(RsConfig), _P, _P, _P, ctypes.c_int32, _P, _P, _P]
         L.rs_phase_profile.restype = ctypes.c_int
         L.rs_phase_profile.argtypes = [_P, ctypes.c_int32]
         L.rs_last_error.restype = ctypes.c_char_p

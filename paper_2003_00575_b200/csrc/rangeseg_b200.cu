@@ -464,6 +464,60 @@ int rs_stage_masks(const rs_config *cfg, const float *d_tables, const float *d_r
     return cuda_check(cudaGetLastError(), "rs_stage_kernel launch");
 }
 
+namespace {
+int stage_launch_args(const rs_config *cfg, const float *d_tables, const float *d_ranges, int32_t batch, KArgs &k,
+                      long long &total, int &blocks) {
+    Plan pl;
+    int st = make_plan(cfg, &pl);
+    if (st) return st;
+    if (batch < 0) return fail(RS_EINVAL, "batch must be >= 0");
+    if (batch > 0 && (!d_tables || !d_ranges)) return fail(RS_EINVAL, "tables and ranges are required");
+    k = pl.kd;
+    k.ranges = d_ranges;
+    k.tables = d_tables;
+    total = (long long)batch * cfg->height * cfg->width;
+    blocks = (int)std::max<long long>(1, std::min<long long>((total + 255) / 256, 148LL * 16));
+    return RS_OK;
+}
+}  // namespace
+
+int rs_height_image(const rs_config *cfg, const float *d_tables, const float *d_ranges, int32_t batch,
+                    float *d_height, void *stream) {
+    KArgs k;
+    long long total;
+    int blocks, st;
+    if ((st = stage_launch_args(cfg, d_tables, d_ranges, batch, k, total, blocks))) return st;
+    if (!total) return RS_OK;
+    if (!d_height) return fail(RS_EINVAL, "height buffer is required");
+    rs::rs_height_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(k, d_height, total);
+    return cuda_check(cudaGetLastError(), "rs_height_kernel launch");
+}
+
+int rs_ground_mask(const rs_config *cfg, const float *d_tables, const float *d_ranges, const float *d_height,
+                   int32_t batch, uint8_t *d_mask, void *stream) {
+    KArgs k;
+    long long total;
+    int blocks, st;
+    if ((st = stage_launch_args(cfg, d_tables, d_ranges, batch, k, total, blocks))) return st;
+    if (!total) return RS_OK;
+    if (!d_height || !d_mask) return fail(RS_EINVAL, "height and mask buffers are required");
+    rs::rs_ground_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(k, d_height, d_mask, total);
+    return cuda_check(cudaGetLastError(), "rs_ground_kernel launch");
+}
+
+int rs_connectivity(const rs_config *cfg, const float *d_tables, const float *d_ranges, const uint8_t *d_mask,
+                    int32_t batch, uint8_t *d_horizontal, uint8_t *d_vertical, void *stream) {
+    KArgs k;
+    long long total;
+    int blocks, st;
+    if ((st = stage_launch_args(cfg, d_tables, d_ranges, batch, k, total, blocks))) return st;
+    if (!total) return RS_OK;
+    if (!d_mask || !d_horizontal || !d_vertical) return fail(RS_EINVAL, "mask and edge buffers are required");
+    rs::rs_connectivity_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(k, d_mask, d_horizontal,
+                                                                                     d_vertical, total);
+    return cuda_check(cudaGetLastError(), "rs_connectivity_kernel launch");
+}
+
 // Host-buffer entry: chunks of frames are pipelined over two streams so the
 // host->device copy of chunk j+1 overlaps the kernel of chunk j and the
 // device->host copy of chunk j-1.
