@@ -42,7 +42,7 @@ constexpr int kMaxRowsFast = 64;              // fast kernel: two seam words
 constexpr size_t kSmemLimit = 227 * 1024 - 4096;
 // kFastOcc fast CTAs per SM: 228 KB per SM, minus 1 KB reserved and the
 // static shared memory of each CTA
-constexpr size_t kFastSmemTarget = 228 * 1024 / rs::kFastOcc - 1024 - 2560;
+constexpr size_t kFastSmemTarget = std::min<size_t>(228 * 1024 / rs::kFastOcc - 1024 - 2560, kSmemLimit);
 constexpr int kMinNodeCap = 512;
 
 thread_local std::string g_err;
