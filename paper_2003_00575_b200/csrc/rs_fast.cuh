@@ -43,6 +43,9 @@ namespace rs {
 #ifndef RS_FAST_THREADS
 #define RS_FAST_THREADS 512
 #endif
+#ifndef RS_STRIP_SETS
+#define RS_STRIP_SETS 4   // step A register sets: 4 = two-row prefetch, 3 = one-row prefetch
+#endif
 constexpr int kFastThreads = RS_FAST_THREADS;
 constexpr int kFastOcc = RS_FAST_OCC;   // CTAs per SM the fast kernel is sized for
 constexpr int kFastWarps = kFastThreads / 32;
@@ -152,19 +155,23 @@ struct RunUF {
 // word ch*4 + j and the left / up edge words are warp-uniform bit operations.
 // The warp walks rows rfirst..rend-1 with the row above in registers and a
 // two-row prefetch; four rotating register sets (unrolled by four) avoid
-// register moves.  Row 0 (whose ground pair is rows 0/1) is done by a
+// register moves (RS_STRIP_SETS=3: one-row prefetch, three sets).  Row 0 (whose ground pair is rows 0/1) is done by a
 // separate ROW0 step.  FULL: the chunk lies inside the row (no load guards,
-// 16-byte stores of the four words by lane 0).
-template <bool FULL, bool MCA>
+// 16-byte stores of the four words by lane 0).  GROUND: ground removal on.
+// Plane stores use 32-bit shared-memory byte addresses (sP/sL/sU: the chunk's
+// words in the band's first row; sPh/sLh: the halo row).
+template <bool FULL, bool MCA, bool GROUND>
 struct BitsStrip {
     const KArgs &a;
     const float *col;
     const float *rowc;
-    uint32_t *P, *L, *U, *Ph, *Lh, *MCp;
+    uint32_t sP, sL, sU, sPh, sLh;
+    uint32_t *MCp;
     int ch, lane, r0, rstart, rend, cb;
-    float thr, tch, mount, keep;
-    bool ground_on;
+    float thr, tch;
     int rfirst;   // first row walked (rstart, or a later row when rows are split between warps)
+    int rowb;     // bytes per row (4 W)
+    int wpb;      // bytes per plane row (4 WPR)
 
     __device__ __forceinline__ void ld4(int r, float (&x)[4], bool pred = true) const {
         const float *p = col + (size_t)r * a.W;
@@ -174,20 +181,21 @@ struct BitsStrip {
             else if (!FULL) x[j] = 0.f;
     }
 
-    // va = row above, v = this row, vb = row below; vn <- row r+2 (PF).
+    // va = row above, v = this row, vb = row below (read by ROW0 only); vn <-
+    // row r + RS_STRIP_SETS - 2 (prefetch; it held row r-2, which MCA reads
+    // first).
     // Stores the raw ballots: presence P, left pair test EH (in the L plane)
     // and up pair test EV (in the U plane); step B masks them with presence
     // one word per thread, 32x cheaper than warp-uniform ops here.
-    template <bool ROW0, bool PF = true>
+    template <bool ROW0, bool HALO = false>
     __device__ __forceinline__ void step(int r, const float (&va)[4], const float (&v)[4], const float (&vb)[4],
                                          float (&vn)[4]) const {
-        // MCA: vn still holds row r-2 until the prefetch below overwrites it
         float v2[4];
         if (MCA) {
 #pragma unroll
             for (int j = 0; j < 4; ++j) v2[j] = vn[j];
         }
-        if (PF) ld4(r + 2, vn, r + 2 < rend);
+        if (!ROW0) ld4(r + RS_STRIP_SETS - 2, vn, r + RS_STRIP_SETS - 2 < rend);
         const float4 c = *reinterpret_cast<const float4 *>(rowc + (r - rstart) * 8);
         const float4 c2 = *reinterpret_cast<const float4 *>(rowc + (r - rstart) * 8 + 4);
         const int srcl = (lane + 31) & 31;
@@ -197,7 +205,7 @@ struct BitsStrip {
         for (int j = 0; j < 4; ++j) {
             const float d1 = ROW0 ? v[j] : va[j];
             const float d2 = ROW0 ? vb[j] : v[j];
-            const bool gr = ground_on & ground_fast(c.x, c.y, c.z, c.w, c2.x, c2.z, d1, d2, v[j], ROW0 ? vb[j] : va[j]);
+            const bool gr = GROUND && ground_fast(c.x, c.y, c.z, c.w, c2.x, c2.z, d1, d2, v[j], ROW0 ? vb[j] : va[j]);
             pw[j] = __ballot_sync(kFull, (v[j] > 0.f) & !gr);
             // left neighbour: lane l-1's cell; lane 0 reads lane 31's cell of
             // word j-1 (word 0 of the chunk: bit 0 is redone in step B)
@@ -206,7 +214,7 @@ struct BitsStrip {
             lw[j] = __ballot_sync(kFull, pair_pass(vl, v[j], tch, thr));
             uw[j] = ROW0 ? 0u : __ballot_sync(kFull, pair_pass(va[j], v[j], c2.y, thr));
         }
-        const bool halo = r < r0;
+        const bool halo = HALO;   // only the first row walked in a band > 0 (peeled in run())
         const int cw = ch * 4;
         if (MCA && !halo) {
             // raw pair tests of the step-A Map Connection offsets: partner
@@ -235,47 +243,99 @@ struct BitsStrip {
                 }
             }
         }
+        const uint32_t off = halo ? 0u : (uint32_t)((r - r0) * wpb);
         if (FULL) {
             if (lane == 0) {
-                const int w = halo ? 0 : (r - r0) * a.WPR + cw;
-                uint32_t *dp = halo ? Ph + cw : P + w, *dl = halo ? Lh + cw : L + w;
-                *reinterpret_cast<uint4 *>(dp) = make_uint4(pw[0], pw[1], pw[2], pw[3]);
-                *reinterpret_cast<uint4 *>(dl) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
-                if (!halo) *reinterpret_cast<uint4 *>(U + w) = make_uint4(uw[0], uw[1], uw[2], uw[3]);
+                sts128((halo ? sPh : sP) + off, pw[0], pw[1], pw[2], pw[3]);
+                sts128((halo ? sLh : sL) + off, lw[0], lw[1], lw[2], lw[3]);
+                if (!halo) sts128(sU + off, uw[0], uw[1], uw[2], uw[3]);
             }
         } else if (lane < 4 && cw + lane < a.WPR) {
             const uint32_t xp = lane == 0 ? pw[0] : lane == 1 ? pw[1] : lane == 2 ? pw[2] : pw[3];
             const uint32_t xl = lane == 0 ? lw[0] : lane == 1 ? lw[1] : lane == 2 ? lw[2] : lw[3];
             const uint32_t xu = lane == 0 ? uw[0] : lane == 1 ? uw[1] : lane == 2 ? uw[2] : uw[3];
-            if (halo) {
-                Ph[cw + lane] = xp;
-                Lh[cw + lane] = xl;
-            } else {
-                const int w = (r - r0) * a.WPR + cw + lane;
-                P[w] = xp;
-                L[w] = xl;
-                U[w] = xu;
-            }
+            const uint32_t lo = off + 4u * (uint32_t)lane;
+            sts32((halo ? sPh : sP) + lo, xp);
+            sts32((halo ? sLh : sL) + lo, xl);
+            if (!halo) sts32(sU + lo, xu);
         }
     }
 
+#if RS_STRIP_SETS == 3
+    // three rotating sets: rows r-1, r and the target of the one-row prefetch
+    __device__ __forceinline__ void run() const {
+        float S0[4], S1[4], S2[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) S0[j] = S1[j] = S2[j] = 0.f;
+        int rf = rfirst;
+        if (rfirst == 0) {   // row 0: ground pair (0, 1), no up edges; band 1 of R = 1: the halo row
+            ld4(0, S1);
+            ld4(1, S2);
+            if (r0 > 0) step<true, true>(0, S0, S1, S2, S0);
+            else step<true>(0, S0, S1, S2, S0);
+            rf = 1;
+        }
+        if (rf >= rend) return;
+        ld4(rf - 1, S0);
+        ld4(rf, S1);
+        if (rf < r0) {
+            // the halo row (first row walked in a band > 0): P / L only
+            step<false, true>(rf, S0, S1, S1, S2);
+            ++rf;
+            if (rf >= rend) return;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {   // (S0, S1, S2) = (r-2, r-1, r) -> (r-1, r, r-2)
+                const float t = S0[j];
+                S0[j] = S1[j];
+                S1[j] = S2[j];
+                S2[j] = t;
+            }
+        } else if (MCA && rf >= 2) {
+            ld4(rf - 2, S2);   // row r-2 of the first step (Map Connections)
+        }
+        for (int r = rf; r < rend; r += 3) {
+            step<false>(r, S0, S1, S1, S2);
+            if (r + 1 >= rend) break;
+            step<false>(r + 1, S1, S2, S2, S0);
+            if (r + 2 >= rend) break;
+            step<false>(r + 2, S2, S0, S0, S1);
+        }
+    }
+#else
+    // four rotating sets: rows r-1, r, r+1 (prefetched) and the target of
+    // the two-row prefetch
     __device__ __forceinline__ void run() const {
         float S0[4], S1[4], S2[4], S3[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) S0[j] = S1[j] = S2[j] = S3[j] = 0.f;
         int rf = rfirst;
-        if (rfirst == 0) {   // row 0: ground pair (0, 1), no up edges
+        if (rfirst == 0) {   // row 0: ground pair (0, 1), no up edges; band 1 of R = 1: the halo row
             ld4(0, S1);
             ld4(1, S2);
-            step<true>(0, S0, S1, S2, S3);
+            if (r0 > 0) step<true, true>(0, S0, S1, S2, S3);
+            else step<true>(0, S0, S1, S2, S3);
             rf = 1;
         }
         if (rf >= rend) return;
-        if (rf >= 1) ld4(rf - 1, S0);
+        ld4(rf - 1, S0);
         ld4(rf, S1);
         ld4(rf + 1, S2, rf + 1 < rend);
-        if (MCA && rf >= 2) ld4(rf - 2, S3);   // row r-2 of the first step (Map Connections)
-        // the first row walked in a band > 0 is the halo row: no up bits needed
+        if (rf < r0) {
+            // the halo row (first row walked in a band > 0): P / L only
+            step<false, true>(rf, S0, S1, S2, S3);
+            ++rf;
+            if (rf >= rend) return;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {   // (r-2, r-1, r, r+1) -> (r-1, r, r+1, r-2)
+                const float t = S0[j];
+                S0[j] = S1[j];
+                S1[j] = S2[j];
+                S2[j] = S3[j];
+                S3[j] = t;
+            }
+        } else if (MCA && rf >= 2) {
+            ld4(rf - 2, S3);   // row r-2 of the first step (Map Connections)
+        }
         for (int r = rf; r < rend; r += 4) {
             step<false>(r, S0, S1, S2, S3);
             if (r + 1 >= rend) break;
@@ -286,6 +346,7 @@ struct BitsStrip {
             step<false>(r + 3, S3, S0, S1, S2);
         }
     }
+#endif
 };
 
 // MCA: some Map Connection offsets (dy <= 2, 0 <= dx <= 31) are tested in
@@ -351,12 +412,19 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
             const int ch = t % nchunk, part = t / nchunk;
             const int rlo = rstart + part * per, rhi = min(rend, rlo + per);
             const int cb = ch * 128 + lane;
-            if (ch * 128 + 128 <= W && (WPR & 3) == 0)
-                BitsStrip<true, MCA>{a, fr + cb, rowc, P, L, U, Ph, Lh, MC, ch, lane, r0, rstart, rhi, cb,
-                                     thr, tch, a.mount, a.keep_above, a.ground != 0, rlo}.run();
-            else
-                BitsStrip<false, MCA>{a, fr + cb, rowc, P, L, U, Ph, Lh, MC, ch, lane, r0, rstart, rhi, cb,
-                                      thr, tch, a.mount, a.keep_above, a.ground != 0, rlo}.run();
+            const uint32_t sb = smem_addr(sm) + 4u * (uint32_t)(ch * 4);
+            const uint32_t sP = sb + 4u * a.o_P, sL = sb + 4u * a.o_L, sU = sb + 4u * a.o_U;
+            const uint32_t sPh = sb + 4u * a.o_Ph, sLh = sb + 4u * a.o_Lh;
+            const bool full = ch * 128 + 128 <= W && (WPR & 3) == 0;
+#define RS_STRIP(F, G)                                                                                     \
+    BitsStrip<F, MCA, G>{a, fr + cb, rowc, sP, sL, sU, sPh, sLh, MC, ch, lane, r0, rstart, rhi, cb, thr, tch, rlo, 4 * W, 4 * WPR} \
+        .run()
+            if (a.ground) {
+                if (full) RS_STRIP(true, true); else RS_STRIP(false, true);
+            } else {
+                if (full) RS_STRIP(true, false); else RS_STRIP(false, false);
+            }
+#undef RS_STRIP
         }
     }
     __syncthreads();
