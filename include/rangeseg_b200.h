@@ -87,14 +87,14 @@ int rs_plan(const rs_config *cfg, int32_t *rows_per_cta, int32_t *ctas_per_frame
  * fast smem, node capacity, dense rows, dense CTAs, dense smem}. */
 int rs_plan_detail(const rs_config *cfg, int32_t *out, int32_t n);
 
-/* Device workspace rs_segment_batch needs for `batch` frames (the overflow
- * list of frames handed from the fast to the dense kernel).  Zero it once
- * after allocation; the library leaves it zeroed after every call.  One
- * workspace per stream. */
+/* Device workspace rs_segment_batch needs for `batch` frames: 0 bytes (the
+ * path needs no scratch beyond the caller's buffers: a frame whose runs
+ * exceed the node capacity is finished in its own label buffer).  Kept for
+ * ABI stability; d_workspace / workspace_size may be NULL / 0. */
 size_t rs_workspace_size(const rs_config *cfg, int32_t batch);
 
 /* B frames, device pointers, enqueued on `stream` (a cudaStream_t; NULL = legacy
- * default stream).  Asynchronous: returns after the launch(es). */
+ * default stream).  One kernel launch; asynchronous: returns after it. */
 int rs_segment_batch(const rs_config *cfg, const float *d_tables, const float *d_ranges,
                      int32_t batch, int32_t *d_labels, int32_t *d_n_clusters,
                      int64_t *d_cluster_sizes, int64_t sizes_stride,

@@ -157,7 +157,7 @@ int max_runs(int R, int W) { return R * W + rs::kFastWarps; }
 
 struct Plan {
     bool fast;            // run rs_fast_kernel (else rs_dense_kernel directly)
-    bool may_overflow;    // fast kernel may hand frames to the dense kernel
+    bool may_overflow;    // a band may exceed the node capacity (fast kernel's overflow path, rs_overflow.cuh)
     KArgs kf, kd;         // arguments of the fast / dense kernels
     size_t smem_f, smem_d;
     int stop_after;       // experiments (rs_config.reserved[1]); 0 in production
@@ -202,7 +202,7 @@ int make_plan(const rs_config *cfg, Plan *pl) {
     // cheaper cluster barriers (measured: 2 bands of 32 rows beat 8 of 8 for
     // 64x2048 frames).  Many Map Connection bit planes shrink the band until
     // the run capacity is at least an eighth of its cells (observed: <= 10% for
-    // 32-row bands of the BASELINE configs; more overflows to the dense kernel).
+    // 32-row bands of the BASELINE configs; more take the overflow path).
     pl->fast = false;
     pl->may_overflow = false;
     pl->smem_f = 0;
@@ -288,102 +288,51 @@ int set_attrs(const Plan &pl) {
 
 template <class Kern>
 int launch_cluster(Kern kern, const KArgs &k, int clusters, int threads, size_t smem, cudaStream_t stream,
-                   const char *what, bool dependent = false) {
+                   const char *what) {
     cudaLaunchConfig_t lc = {};
     lc.gridDim = dim3((unsigned)(clusters * k.C), 1, 1);
     lc.blockDim = dim3((unsigned)threads, 1, 1);
     lc.dynamicSmemBytes = smem;
     lc.stream = stream;
-    cudaLaunchAttribute at[2];
+    cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = (unsigned)k.C;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
-    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[1].val.programmaticStreamSerializationAllowed = 1;
     lc.attrs = at;
-    lc.numAttrs = dependent ? 2 : 1;
+    lc.numAttrs = 1;
     return cuda_check(cudaLaunchKernelEx(&lc, kern, k), what);
 }
 
-// Clusters of the dense kernel that are co-resident in one wave: the
-// overflow pass uses that many persistent clusters, so a batch in which every
-// frame overflows still fills the GPU (an empty list costs the same).
-int dense_wave_clusters(const Plan &pl) {
-    static std::mutex mu;
-    static int dev_c = -1, C_c = 0, n_c = 0;
-    static size_t smem_c = 0;
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess) return 32 / pl.kd.C;
-    std::lock_guard<std::mutex> g(mu);
-    if (dev == dev_c && C_c == pl.kd.C && smem_c == pl.smem_d) return n_c;
-    cudaLaunchConfig_t lc = {};
-    lc.gridDim = dim3((unsigned)pl.kd.C, 1, 1);
-    lc.blockDim = dim3((unsigned)rs::kDenseThreads, 1, 1);
-    lc.dynamicSmemBytes = pl.smem_d;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = (unsigned)pl.kd.C;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    lc.attrs = at;
-    lc.numAttrs = 1;
-    int n = 0;
-    if (cudaOccupancyMaxActiveClusters(&n, rs::rs_dense_kernel, &lc) != cudaSuccess || n < 1) {
-        cudaGetLastError();
-        n = std::max(1, 32 / pl.kd.C);
-    }
-    dev_c = dev;
-    C_c = pl.kd.C;
-    smem_c = pl.smem_d;
-    n_c = n;
-    return n;
-}
-
+// One launch per batch: rs_fast_kernel (frames whose bands overflow the node
+// capacity are finished by the same kernel, rs_overflow.cuh), or
+// rs_dense_kernel when the fast plan cannot hold the geometry.
 int segment_launch(const Plan &pl, const float *d_tables, const float *d_ranges, int32_t batch, int32_t *d_labels,
-                   int32_t *d_n_clusters, int64_t *d_cluster_sizes, int64_t sizes_stride, int *ws,
-                   cudaStream_t stream) {
+                   int32_t *d_n_clusters, int64_t *d_cluster_sizes, int64_t sizes_stride, cudaStream_t stream) {
     int st = set_attrs(pl);
     if (st) return st;
-    KArgs kd = pl.kd;
-    kd.ranges = d_ranges;
-    kd.tables = d_tables;
-    kd.labels = d_labels;
-    kd.ncl = d_n_clusters;
-    kd.sizes = d_cluster_sizes;
-    kd.sizes_stride = sizes_stride;
-    kd.use_tma = (pl.kd.W % 4 == 0) && ((reinterpret_cast<uintptr_t>(d_ranges) & 15u) == 0);
-    kd.ws = ws;
+    KArgs k = pl.fast ? pl.kf : pl.kd;
+    k.ranges = d_ranges;
+    k.tables = d_tables;
+    k.labels = d_labels;
+    k.ncl = d_n_clusters;
+    k.sizes = d_cluster_sizes;
+    k.sizes_stride = sizes_stride;
     if (!pl.fast) {
-        kd.list_mode = 0;
-        return launch_cluster(rs::rs_dense_kernel, kd, batch, rs::kDenseThreads, pl.smem_d, stream,
+        k.use_tma = (pl.kd.W % 4 == 0) && ((reinterpret_cast<uintptr_t>(d_ranges) & 15u) == 0);
+        return launch_cluster(rs::rs_dense_kernel, k, batch, rs::kDenseThreads, pl.smem_d, stream,
                               "rs_dense_kernel launch");
     }
-    KArgs kf = pl.kf;
-    kf.ranges = d_ranges;
-    kf.tables = d_tables;
-    kf.labels = d_labels;
-    kf.ncl = d_n_clusters;
-    kf.sizes = d_cluster_sizes;
-    kf.sizes_stride = sizes_stride;
-    kf.ws = ws;
-    kf.stop_after = pl.stop_after;
-    st = kf.n_aoff > 0
-             ? launch_cluster(rs::rs_fast_kernel<true>, kf, batch, rs::kFastThreads, pl.smem_f, stream,
-                              "rs_fast_kernel launch")
-             : launch_cluster(rs::rs_fast_kernel<false>, kf, batch, rs::kFastThreads, pl.smem_f, stream,
-                              "rs_fast_kernel launch");
-    if (st || !pl.may_overflow) return st;
-    // Overflow pass: a few persistent clusters walk the (usually empty) list;
-    // a programmatic dependent launch hides its launch latency behind the
-    // fast kernel's tail.
-    kd.list_mode = 1;
-    const int G = std::max(1, std::min<int>(batch, dense_wave_clusters(pl)));
-    return launch_cluster(rs::rs_dense_kernel, kd, G, rs::kDenseThreads, pl.smem_d, stream,
-                          "rs_dense_kernel (overflow) launch", true);
+    k.stop_after = pl.stop_after;
+    return k.n_aoff > 0 ? launch_cluster(rs::rs_fast_kernel<true>, k, batch, rs::kFastThreads, pl.smem_f, stream,
+                                         "rs_fast_kernel launch")
+                        : launch_cluster(rs::rs_fast_kernel<false>, k, batch, rs::kFastThreads, pl.smem_f, stream,
+                                         "rs_fast_kernel launch");
 }
 
-size_t workspace_bytes(int32_t batch) { return (size_t)(2 + std::max(batch, 0)) * sizeof(int); }
+// No device workspace is needed any more (the overflow path works in the label
+// buffer); the ABI keeps the workspace arguments, which are ignored.
+size_t workspace_bytes(int32_t) { return 0; }
 
 }  // namespace
 
@@ -440,10 +389,10 @@ int rs_segment_batch(const rs_config *cfg, const float *d_tables, const float *d
                                        std::to_string(need));
     }
     if ((long long)batch * std::max(pl.kf.C, pl.kd.C) > 0x7fffffffLL) return fail(RS_EINVAL, "batch too large");
-    if (pl.fast && pl.may_overflow && (!d_workspace || workspace_size < workspace_bytes(batch)))
-        return fail(RS_EINVAL, "a zero-initialised workspace of rs_workspace_size() bytes is required");
+    (void)d_workspace;
+    (void)workspace_size;
     return segment_launch(pl, d_tables, d_ranges, batch, d_labels, d_n_clusters, d_cluster_sizes, sizes_stride,
-                          static_cast<int *>(d_workspace), static_cast<cudaStream_t>(stream));
+                          static_cast<cudaStream_t>(stream));
 }
 
 int rs_stage_masks(const rs_config *cfg, const float *d_tables, const float *d_ranges, int32_t batch,
@@ -530,8 +479,7 @@ struct HostCtx {
     // kHostStreams streams round-robin over chunks, so the host->device copy
     // of chunk j+2 can run while chunk j is copied back (both copy engines busy)
     static constexpr int kHostStreams = 4;
-    int *d_ws[kHostStreams] = {};
-    size_t cap_frames = 0, cap_tables = 0, cap_sizes = 0, frame_cells = 0, cap_ws = 0;
+    size_t cap_frames = 0, cap_tables = 0, cap_sizes = 0, frame_cells = 0;
     cudaStream_t s[kHostStreams] = {};
     int device = -1;
 };
@@ -574,8 +522,6 @@ int rs_segment_batch_host(const rs_config *cfg, const float *h_tables, const flo
         g_host.cap_tables = 0;
         cudaFree(g_host.d_tables);
         g_host.d_tables = nullptr;
-        for (auto &w : g_host.d_ws) { cudaFree(w); w = nullptr; }
-        g_host.cap_ws = 0;
     }
     const size_t HW = (size_t)cfg->height * cfg->width;
     const size_t nt = rs_tables_count(cfg->height, cfg->n_offsets);
@@ -592,17 +538,6 @@ int rs_segment_batch_host(const rs_config *cfg, const float *h_tables, const flo
             return st;
         g_host.cap_frames = batch;
         g_host.cap_sizes = h_cluster_sizes ? (size_t)batch * sizes_stride : 0;
-    }
-    const size_t wsb = workspace_bytes(batch);
-    if (g_host.cap_ws < wsb) {
-        for (auto &w : g_host.d_ws) {
-            cudaFree(w);
-            w = nullptr;
-            if ((st = cuda_check(cudaMalloc(&w, wsb), "cudaMalloc workspace")) ||
-                (st = cuda_check(cudaMemset(w, 0, wsb), "cudaMemset workspace")))
-                return st;
-        }
-        g_host.cap_ws = wsb;
     }
     if (g_host.cap_tables < nt) {
         cudaFree(g_host.d_tables);
@@ -626,8 +561,7 @@ int rs_segment_batch_host(const rs_config *cfg, const float *h_tables, const flo
                                              cudaMemcpyHostToDevice, s), "copy ranges")))
             break;
         st = segment_launch(pl, g_host.d_tables, g_host.d_ranges + off, nb, g_host.d_labels + off, g_host.d_ncl + b0,
-                            h_cluster_sizes ? g_host.d_sizes + (size_t)b0 * sizes_stride : nullptr, sizes_stride,
-                            g_host.d_ws[j % HostCtx::kHostStreams], s);
+                            h_cluster_sizes ? g_host.d_sizes + (size_t)b0 * sizes_stride : nullptr, sizes_stride, s);
         if (st) break;
         if ((st = cuda_check(cudaMemcpyAsync(h_labels + off, g_host.d_labels + off, nb * HW * 4,
                                              cudaMemcpyDeviceToHost, s), "copy labels")))

@@ -36,8 +36,6 @@ struct KArgs {
     int o_P, o_L, o_U, o_SB, o_RS, o_Ph, o_Lh, o_MC, o_TL, o_LR, o_K, o_E, o_SZ;
     int NC, SHN;                  // fast kernel: run-node capacity per band, id bits
     int use_tma;                  // dense kernel: stage rows with TMA bulk copies
-    int *ws;                      // [0] overflow count, [1] done counter, [2..] frame list
-    int list_mode;                // dense kernel: process the overflow list
     int stop_after;               // experiments only: leave the fast kernel after phase N (0 = never)
     int udyn;                     // fast kernel: dynamic edge grabbing in the local unions (clusters of >= 4 bands)
     int n_aoff;                   // Map Connection offsets evaluated in step A (dy <= 2, 0 <= dx <= 31), at most 4

@@ -582,37 +582,14 @@ __device__ __forceinline__ void dense_frame(const KArgs &a, uint32_t *sm, DenseS
 
 
 // Dense kernel: every band cell owns a union-find slot (no capacity limit).
-// Runs directly over a batch (list_mode == 0) or, after the fast kernel, over
-// the frames it could not hold (list_mode == 1; a persistent loop of
-// gridDim.x / C clusters over the overflow list in ws).
+// Runs over a batch when the fast plan cannot hold the geometry.
 __global__ void __launch_bounds__(kDenseThreads, 1) rs_dense_kernel(const __grid_constant__ KArgs a) {
     extern __shared__ __align__(128) uint32_t sm[];
     __shared__ __align__(8) uint64_t mbar;
     __shared__ DenseShared sh;
     if (threadIdx.x == 0 && a.use_tma) mbar_init(&mbar, 1);
     __syncthreads();
-    const int cid = blockIdx.x / a.C;
-    if (!a.list_mode) {
-        dense_frame(a, sm, sh, &mbar, cid, 0);
-        return;
-    }
-    cg::cluster_group cl = cg::this_cluster();
-    // launched as a programmatic dependent of rs_fast_kernel: wait until its
-    // grid has completed and its writes (the overflow list) are visible
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-    const int G = gridDim.x / a.C;
-    const int count = *reinterpret_cast<volatile int *>(a.ws);
-    uint32_t it = 0;
-    for (int j = cid; j < count; j += G, ++it)
-        dense_frame(a, sm, sh, &mbar, a.ws[2 + j], it & 1u);
-    cl.sync();
-    if (cl.block_rank() == 0 && threadIdx.x == 0) {
-        __threadfence();
-        if (atomicAdd(a.ws + 1, 1) == G - 1) {   // last cluster out resets the list
-            a.ws[0] = 0;
-            a.ws[1] = 0;
-        }
-    }
+    dense_frame(a, sm, sh, &mbar, blockIdx.x / a.C, 0);
 }
 
 }  // namespace rs

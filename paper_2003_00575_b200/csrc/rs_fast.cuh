@@ -28,12 +28,13 @@
 //   L  run labels from the root's band (DSMEM), then per-cell labels with
 //      16-byte streaming stores.
 //
-// A band with more runs than the node capacity NC marks the frame; the whole
-// cluster then leaves and the frame is appended to the overflow list, which
-// rs_dense_kernel processes right after (a programmatic dependent launch).
+// A band with more runs than the node capacity NC marks the frame; after
+// barrier #1 the whole cluster then labels it with a union-find over cells in
+// global memory (rs_overflow.cuh), so no second launch is ever needed.
 #pragma once
 
 #include "rs_common.cuh"
+#include "rs_overflow.cuh"
 
 namespace rs {
 
@@ -358,6 +359,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
     __shared__ uint32_t warp_tot[kFastWarps];
     __shared__ uint32_t cta_cnt, cta_sum, ovf, ovf_any, n_edges, n_xedges, ucur;
     __shared__ uint32_t cta_pre[16];   // label base of every band of the cluster
+    __shared__ uint32_t ovf_cnt[2];    // overflow path: kept roots and their cells in this band
     __shared__ uint32_t seam[2];   // seam edge per own row (R <= 64)
     __shared__ __align__(16) float rowc[(64 + 1) * 8];   // per-row constants of the band
 
@@ -821,10 +823,8 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
         ovf_any = any;
     }
     __syncthreads();
-    if (ovf_any) {   // cluster-uniform: the dense kernel takes this frame
-        if (k == 0 && tid == 0) a.ws[2 + atomicAdd(a.ws, 1)] = frame;
-        cl.sync();
-        asm volatile("griddepcontrol.launch_dependents;");
+    if (ovf_any) {   // cluster-uniform: union-find over cells in global memory (rs_overflow.cuh)
+        overflow_frame(a, P, L, U, MC, seam, ovf_cnt, warp_tot, frame);
         return;
     }
 
@@ -1048,8 +1048,6 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
         }
     }
     RS_MARK(15);
-    // let the overflow pass (a programmatic dependent launch) get scheduled
-    asm volatile("griddepcontrol.launch_dependents;");
 }
 
 }  // namespace rs

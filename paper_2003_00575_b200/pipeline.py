@@ -137,11 +137,11 @@ class Pipeline:
         self.rs_config = _native.make_config(self.packed, rows_per_cta, node_capacity)
         self.rows_per_cta, self.ctas_per_frame, self.smem_bytes = _native.plan(self.rs_config)
         self.plan = _native.plan_detail(self.rs_config)
-        self._workspaces = {}
         self.device = torch.device(device if device is not None else "cuda")
         if self.device.type == "cuda" and self.device.index is None and torch.cuda.is_available():
             self.device = torch.device("cuda", torch.cuda.current_device())
         self._tables = None
+        self._workspaces = {}
         self._tables_host = np.ascontiguousarray(self.packed.block, dtype=np.float32)
 
     # -- helpers -----------------------------------------------------------
@@ -164,14 +164,16 @@ class Pipeline:
             self._tables = torch.from_numpy(self._tables_host).to(self.device)
         return self._tables
 
-    def workspace(self, batch: int, stream) -> torch.Tensor:
-        """Zero-initialised device workspace, one per stream (the overflow list)."""
+    def _workspace(self, batch: int, stream):
+        """Device workspace the library asks for (none: rs_workspace_size is 0
+        for this library; kept so the ABI's workspace contract stays honoured)."""
         need = int(_native.lib().rs_workspace_size(ctypes.byref(self.rs_config), batch))
-        key = stream.cuda_stream
-        ws = self._workspaces.get(key)
+        if need <= 0:
+            return None
+        ws = self._workspaces.get(stream.cuda_stream)
         if ws is None or ws.numel() < need:
-            ws = torch.zeros(max(need, 8), dtype=torch.uint8, device=self.device)
-            self._workspaces[key] = ws
+            ws = torch.zeros(need, dtype=torch.uint8, device=self.device)
+            self._workspaces[stream.cuda_stream] = ws
         return ws
 
     def _check_frames(self, ranges: torch.Tensor):
@@ -206,11 +208,11 @@ class Pipeline:
             cluster_sizes = None
         stride = cluster_sizes.shape[1] if cluster_sizes is not None else 0
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
-        ws = self.workspace(B, s)
+        ws = self._workspace(B, s)
         st = _native.lib().rs_segment_batch(
             ctypes.byref(self.rs_config), _ptr(self.device_tables()), _ptr(ranges), B,
             _ptr(labels), _ptr(n_clusters), _ptr(cluster_sizes), stride,
-            _ptr(ws), ws.numel(), ctypes.c_void_p(s.cuda_stream))
+            _ptr(ws), 0 if ws is None else ws.numel(), ctypes.c_void_p(s.cuda_stream))
         _native.check(st, "rs_segment_batch")
         return BatchResult(labels, n_clusters, cluster_sizes)
 

@@ -303,12 +303,13 @@ def test_batch_zero_and_errors(cuda):
         pipe.segment_batch(torch.zeros((1, 32, 1024), device="cuda:0", dtype=torch.float64))
 
 
-# ------------------------------------------------- overflow -> dense kernel ---
+# ------------------------------------------- node-capacity overflow path -----
 @pytest.mark.parametrize("cap", [32, 700, 2000])
 @pytest.mark.parametrize("cid,variant", [(1, "default"), (4, "core"), (3, "S1")])
-def test_node_capacity_overflow_goes_to_dense_kernel(cap, cid, variant, config_frames):
-    """Frames whose bands hold more runs than the node capacity are handed to
-    the dense kernel through the overflow list; results must not change."""
+def test_node_capacity_overflow_path(cap, cid, variant, config_frames):
+    """Frames whose bands hold more runs than the node capacity are finished by
+    the fast kernel's global-memory union-find over cells (rs_overflow.cuh);
+    results must not change."""
     model = synthetic.sensor_for(synthetic.CONFIGS[cid])
     cfg = VARIANTS[variant]
     frames = config_frames[cid]
@@ -316,7 +317,7 @@ def test_node_capacity_overflow_goes_to_dense_kernel(cap, cid, variant, config_f
     assert pipe.plan["fast"] and pipe.plan["may_overflow"]
     want_l, want_n, want_s = oracle.segment_batch(frames.cpu().numpy(), pipe.packed,
                                                   sizes_stride=pipe.sizes_stride)
-    for _ in range(2):    # the overflow list must be reset between calls
+    for _ in range(2):    # repeat calls: nothing carried over between them
         res = pipe.segment_batch(frames)
         torch.cuda.synchronize()
         assert np.array_equal(res.n_clusters.cpu().numpy(), want_n)
@@ -325,5 +326,30 @@ def test_node_capacity_overflow_goes_to_dense_kernel(cap, cid, variant, config_f
         for b in range(frames.shape[0]):
             k = int(want_n[b])
             assert np.array_equal(got_s[b, :k + 1], want_s[b, :k + 1])
-    ws = pipe.workspace(frames.shape[0], torch.cuda.current_stream())
-    assert int(ws[:8].view(torch.int32)[:2].abs().sum()) == 0
+
+
+@pytest.mark.parametrize("variant", ["default", "core", "S1"])
+def test_natural_overflow_noise_frames(variant):
+    """Frames of independent random ranges: almost every cell is its own run,
+    far above the node capacity, mixed with ordinary frames in one batch."""
+    spec = synthetic.CONFIGS[1]
+    model = synthetic.sensor_for(spec)
+    g = np.random.default_rng(11)
+    H, W = spec.H, spec.W
+    noise = g.uniform(1.0, 60.0, size=(3, H, W)).astype(np.float32)
+    noise[1, : H // 2] = 0.0                       # only the lower band overflows
+    noise[2, H // 2:] = np.float32(7.5)             # upper band overflows, lower band one component
+    frames = torch.cat([synthetic.make_batch(1, 2, device="cuda:0"),
+                        torch.from_numpy(noise).cuda()])
+    pipe = rs.Pipeline(model, VARIANTS[variant], device="cuda:0")
+    assert pipe.plan["may_overflow"]
+    want_l, want_n, want_s = oracle.segment_batch(frames.cpu().numpy(), pipe.packed,
+                                                  sizes_stride=pipe.sizes_stride)
+    res = pipe.segment_batch(frames)
+    torch.cuda.synchronize()
+    assert np.array_equal(res.n_clusters.cpu().numpy(), want_n)
+    assert np.array_equal(res.labels.cpu().numpy(), want_l)
+    got_s = res.cluster_sizes.cpu().numpy()
+    for b in range(frames.shape[0]):
+        k = int(want_n[b])
+        assert np.array_equal(got_s[b, :k + 1], want_s[b, :k + 1])
