@@ -1007,7 +1007,11 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
     }
     if (a.stop_after == 8) { cl.sync(); return; }
     RS_MARK(13);
-    cl.sync();   // #5: no DSMEM access after this point
+    // #5, split: arrive now (this CTA reads no other CTA's shared memory after
+    // this point), wait just before exiting (no CTA may exit while another
+    // still reads its shared memory), so the wait overlaps the cell sweep
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+    __syncthreads();   // run labels (SZ) of this band are complete
 
     RS_MARK(14);
     int32_t *out = a.labels + (size_t)frame * H * W + (size_t)r0 * W;
@@ -1048,6 +1052,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
         }
     }
     RS_MARK(15);
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
 }  // namespace rs
