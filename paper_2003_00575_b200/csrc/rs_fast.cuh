@@ -824,7 +824,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
     }
     __syncthreads();
     if (ovf_any) {   // cluster-uniform: union-find over cells in global memory (rs_overflow.cuh)
-        overflow_frame(a, P, L, U, MC, seam, ovf_cnt, warp_tot, frame);
+        overflow_frame(a, P, L, U, Lh, MC, seam, ovf_cnt, warp_tot, frame);
         return;
     }
 

@@ -11,11 +11,12 @@
 // min_points cells, label = 1 + rank, 0 = background / dropped.
 //
 // Entry encodings in the parent array during the passes:
-//   absent cell          kAbsent (INT_MIN)
-//   F2-F3 present cell   parent cell index (>= 0); a root points to itself
+//   absent cell          kAbsent (INT_MIN; F1-F6)
+//   F1-F3 present cell   parent cell index (>= 0); a root points to itself
 //   F4-F5 root           -(number of cells counted so far)
 //   F6    root           -(label + 1)   (label 0 = dropped)
-// and finally every cell holds its label.
+// and finally every cell holds its label.  Every present cell starts at the
+// first cell of its run (F1), so left edges need no unions.
 //
 // Rare by construction (the planner sizes the node capacity above every
 // BASELINE frame), so this path favours simplicity over speed: one relaxed
@@ -32,6 +33,9 @@ constexpr int kAbsent = INT_MIN;
 #define RS_OVF_INLINE __forceinline__   // measured: inlined beats a call (config 1 -1%, config 3 -2%)
 #endif
 
+// Relaxed gpu-scope accesses: coherent with the atomics (no stale L1 line of
+// an entry another CTA of the cluster updated), and never merged or hoisted
+// by the compiler across the union-find loops.
 __device__ __forceinline__ int ldg_relaxed(const int *p) {
     int v;
     asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -77,72 +81,113 @@ __device__ __forceinline__ void ovf_unite(int *par, int x, int y) {
 }
 
 // Called by every thread of every CTA of the cluster (cluster-uniform branch).
-// P/L/U/MC: this band's planes (shared memory); seamw: this band's seam bits;
-// cnt: two shared words of this CTA published to the cluster.
+// P/L/U/MC: this band's planes (shared memory); Lh: the halo row's left
+// edges; seamw: this band's seam bits; cnt: two shared words of this CTA
+// published to the cluster; wtot: one shared word per warp.
+//
+// Passes walk the band word by word, a warp per word and a lane per cell, so
+// every global access of a warp is one coalesced 128-byte row segment.
 __device__ RS_OVF_INLINE void overflow_frame(const KArgs &a, const uint32_t *P, const uint32_t *L, const uint32_t *U,
-                                            const uint32_t *MC, const uint32_t *seamw, uint32_t *cnt, uint32_t *wtot,
-                                            int frame) {
+                                             const uint32_t *Lh, const uint32_t *MC, const uint32_t *seamw, uint32_t *cnt,
+                                             uint32_t *wtot, int frame) {
     cg::cluster_group cl = cg::this_cluster();
     const int k = (int)cl.block_rank();
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int nthr = blockDim.x, nwarp = nthr >> 5;
+    const int nwarp = blockDim.x >> 5;
     const int H = a.H, W = a.W, WPR = a.WPR;
     const int r0 = k * a.R, rows = min(a.R, H - r0);
-    const int n = rows * W, g0 = r0 * W;   // band cells, first cell index
+    const int g0 = r0 * W;   // first cell of the band
     int *par = a.labels + (size_t)frame * H * W;
-    auto bit = [&](const uint32_t *pl, int i) -> bool {   // band cell i of a plane
-        const int q = i / W, c = i - q * W;
-        return (pl[q * WPR + (c >> 5)] >> (c & 31)) & 1u;
-    };
+    const uint32_t lt = (1u << lane) - 1u;
 
-    // F1: every present cell is its own root
-    for (int i = tid; i < n; i += nthr) stg_relaxed(par + g0 + i, bit(P, i) ? g0 + i : kAbsent);
+    // F1: every present cell points to the first cell of its run (runs are
+    // the left-linked segments of a row); a warp walks one row's words
+    for (int q = warp; q < rows; q += nwarp) {
+        int carry = 0;   // first cell of the run entering the current word
+        for (int cw = 0; cw < WPR; ++cw) {
+            const int w = q * WPR + cw, c = cw * 32 + lane;
+            const uint32_t pw = P[w], ts = pw & ~L[w];   // true run starts
+            const uint32_t m = ts & (lt | (1u << lane));
+            const int start = m ? cw * 32 + 31 - __clz(m) : carry;
+            if (c < W) stg_relaxed(par + g0 + q * W + c, ((pw >> lane) & 1u) ? g0 + q * W + start : kAbsent);
+            if (ts) carry = cw * 32 + 31 - __clz(ts);
+        }
+    }
     cl.sync();
-    // F2: unite along every edge (left, up, seam, Map Connections)
-    for (int i = tid; i < n; i += nthr) {
-        if (!bit(P, i)) continue;
-        const int q = i / W, c = i - q * W, g = g0 + i, r = r0 + q;
-        if (bit(L, i)) ovf_unite(par, g, g - 1);
-        if (bit(U, i)) ovf_unite(par, g, g - W);
-        if (c == 0 && W > 1 && ((seamw[q >> 5] >> (q & 31)) & 1u)) ovf_unite(par, g, r * W + W - 1);
+    // F2: unite along the up edges that the left neighbour's up edge does not
+    // already imply, the seam and the Map Connection edges
+    for (int w = warp; w < rows * WPR; w += nwarp) {
+        const int q = w / WPR, cw = w - q * WPR, c = cw * 32 + lane;
+        const int g = g0 + q * W + c, r = r0 + q;
+        const uint32_t uw = U[w];
+        if (uw) {
+            const uint32_t lw = L[w], la = q > 0 ? L[w - WPR] : Lh[cw];
+            const uint32_t uprev = (uw << 1) | (cw > 0 ? U[w - 1] >> 31 : 0u);
+            if (((uw & ~(uprev & lw & la)) >> lane) & 1u) ovf_unite(par, g, g - W);
+        }
+        if (cw == 0 && lane == 0 && W > 1 && ((seamw[q >> 5] >> (q & 31)) & 1u)) ovf_unite(par, g, r * W + W - 1);
         for (int o = 0; o < a.n_off; ++o) {
-            if (!bit(MC + o * a.nwords, i)) continue;
+            if (!((MC[o * a.nwords + w] >> lane) & 1u)) continue;
             int tc = (c - a.dx[o]) % W;
             if (tc < 0) tc += W;
             ovf_unite(par, g, (r - a.dy[o]) * W + tc);
         }
     }
     cl.sync();
-    // F3: flatten; every store writes a root, so a concurrent reader of an
-    // entry sees its old parent or its root (both ancestors)
-    for (int i = tid; i < n; i += nthr) {
-        const int g = g0 + i;
-        if (ldg_relaxed(par + g) != kAbsent) stg_relaxed(par + g, ovf_root(par, g));
+    // F3: flatten.  Only run starts are ever roots or parents (every other
+    // cell points to its run start from F1, and hooks and path halving only
+    // ever target roots / ancestors), so first the starts take their root
+    // (read-only finds: a path-halving store here could overwrite another
+    // thread's finished entry), then every other cell its start's root.
+    for (int w = warp; w < rows * WPR; w += nwarp) {
+        const int q = w / WPR, cw = w - q * WPR, g = g0 + q * W + cw * 32 + lane;
+        if (((P[w] & ~L[w]) >> lane) & 1u) stg_relaxed(par + g, ovf_root(par, g));
     }
     cl.sync();
-    // F4: roots start their count (themselves)
-    for (int i = tid; i < n; i += nthr)
-        if (ldg_relaxed(par + g0 + i) == g0 + i) stg_relaxed(par + g0 + i, -1);
-    cl.sync();
-    // F5: every other present cell counts itself at its root
-    for (int i = tid; i < n; i += nthr) {
-        const int p = ldg_relaxed(par + g0 + i);
-        if (p >= 0) atomicAdd(par + p, -1);
+    for (int w = warp; w < rows * WPR; w += nwarp) {
+        const int q = w / WPR, cw = w - q * WPR, g = g0 + q * W + cw * 32 + lane;
+        if (((P[w] & L[w]) >> lane) & 1u) stg_relaxed(par + g, ldg_relaxed(par + ldg_relaxed(par + g)));
     }
     cl.sync();
-    // F6: kept roots ranked in cell order: warp w owns cells [w*per, (w+1)*per)
+    // F4: roots start their count (themselves: -1) ...
+    for (int w = warp; w < rows * WPR; w += nwarp) {
+        const int q = w / WPR, cw = w - q * WPR, g = g0 + q * W + cw * 32 + lane;
+        if (((P[w] >> lane) & 1u) && ldg_relaxed(par + g) == g) stg_relaxed(par + g, -1);
+    }
+    cl.sync();
+    // F5: ... and every other present cell counts itself there, one atomic
+    // per root and word (lanes grouped by root; a root's entry is < 0, every
+    // other present entry is its root's index >= 0)
+    for (int w = warp; w < rows * WPR; w += nwarp) {
+        const int q = w / WPR, cw = w - q * WPR, g = g0 + q * W + cw * 32 + lane;
+        const int v = ((P[w] >> lane) & 1u) ? ldg_relaxed(par + g) : -1;
+        const bool member = v >= 0;
+        const uint32_t grp = __match_any_sync(kFull, member ? v : -1);
+        if (member && lane == __ffs(grp) - 1) atomicAdd(par + v, -__popc(grp));
+    }
+    cl.sync();
+    // F6: kept roots ranked in cell order: warp w owns words [w*per, (w+1)*per)
     const uint32_t minp = a.min_points > 1 ? (uint32_t)a.min_points : 1u;
-    const int per = ((n + nwarp - 1) / nwarp + 31) & ~31;
-    const int c0 = min(warp * per, n), c1 = min(c0 + per, n);
+    const int nw = rows * WPR;
+    const int per = (nw + nwarp - 1) / nwarp;
+    const int w0 = min(warp * per, nw), w1 = min(w0 + per, nw);
+    auto root_size = [&](int w, int &g) -> int {   // size of the root at this lane's cell, else 0
+        const int q = w / WPR, cw = w - q * WPR;
+        g = g0 + q * W + cw * 32 + lane;
+        if (!((P[w] >> lane) & 1u)) return 0;
+        const int v = ldg_relaxed(par + g);
+        return v < 0 ? -v : 0;   // roots hold -(size); other cells their root (>= 0)
+    };
     uint32_t wk = 0;
     unsigned long long wsum = 0;
-    for (int i = c0 + lane; i - lane < c1; i += 32) {
-        const int v = i < c1 ? ldg_relaxed(par + g0 + i) : kAbsent;
-        const bool kept = v != kAbsent && v < 0 && (uint32_t)(-v) >= minp;
+    for (int w = w0; w < w1; ++w) {
+        int g;
+        const int sz = root_size(w, g);
+        const bool kept = sz > 0 && (uint32_t)sz >= minp;
         wk += __popc(__ballot_sync(kFull, kept));
-        unsigned long long s = kept ? (unsigned long long)(-v) : 0ull;
-        for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(kFull, s, off);
-        wsum += s;
+        unsigned long long sv = kept ? (unsigned long long)sz : 0ull;
+        for (int off = 16; off; off >>= 1) sv += __shfl_xor_sync(kFull, sv, off);
+        wsum += sv;
     }
     if (lane == 0) wtot[warp] = wk;
     __syncthreads();
@@ -167,33 +212,41 @@ __device__ RS_OVF_INLINE void overflow_frame(const KArgs &a, const uint32_t *P, 
         if (a.ncl) a.ncl[frame] = (int32_t)tot;
         if (a.sizes) a.sizes[(size_t)frame * a.sizes_stride] = (int64_t)H * W - (int64_t)sum;
     }
+    // roots: entry -> -(label + 1), label 0 = dropped
     uint32_t run = base + wtot[warp];
-    for (int i = c0 + lane; i - lane < c1; i += 32) {
-        const int v = i < c1 ? ldg_relaxed(par + g0 + i) : kAbsent;
-        const bool root = v != kAbsent && v < 0;
-        const bool kept = root && (uint32_t)(-v) >= minp;
+    for (int w = w0; w < w1; ++w) {
+        int g;
+        const int sz = root_size(w, g);
+        const bool kept = sz > 0 && (uint32_t)sz >= minp;
         const uint32_t m = __ballot_sync(kFull, kept);
-        if (root) {
+        if (sz > 0) {
             uint32_t label = 0;
             if (kept) {
-                label = run + __popc(m & ((1u << lane) - 1u)) + 1u;
-                if (a.sizes) a.sizes[(size_t)frame * a.sizes_stride + label] = (int64_t)(-v);
+                label = run + __popc(m & lt) + 1u;
+                if (a.sizes) a.sizes[(size_t)frame * a.sizes_stride + label] = (int64_t)sz;
             }
-            stg_relaxed(par + g0 + i, -(int)label - 1);
+            stg_relaxed(par + g, -(int)label - 1);
         }
         run += __popc(m);
     }
     cl.sync();
     // F7: cells that are not roots take their root's label; absent cells 0
-    for (int i = tid; i < n; i += nthr) {
-        const int g = g0 + i, p = ldg_relaxed(par + g);
-        if (p == kAbsent) stg_relaxed(par + g, 0);
-        else if (p >= 0) stg_relaxed(par + g, -ldg_relaxed(par + p) - 1);
+    for (int w = warp; w < rows * WPR; w += nwarp) {
+        const int q = w / WPR, cw = w - q * WPR, c = cw * 32 + lane, g = g0 + q * W + c;
+        if (c >= W) continue;
+        if (!((P[w] >> lane) & 1u)) {
+            stg_relaxed(par + g, 0);
+        } else {
+            const int p = ldg_relaxed(par + g);
+            if (p >= 0) stg_relaxed(par + g, -ldg_relaxed(par + p) - 1);
+        }
     }
     cl.sync();
     // F8: roots decode their own label
-    for (int i = tid; i < n; i += nthr) {
-        const int g = g0 + i, p = ldg_relaxed(par + g);
+    for (int w = warp; w < rows * WPR; w += nwarp) {
+        const int q = w / WPR, cw = w - q * WPR, g = g0 + q * W + cw * 32 + lane;
+        if (!((P[w] >> lane) & 1u)) continue;
+        const int p = ldg_relaxed(par + g);
         if (p < 0) stg_relaxed(par + g, -p - 1);
     }
 }

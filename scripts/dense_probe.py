@@ -1,4 +1,4 @@
-"""Throughput when every frame takes the dense (overflow) kernel (experiments)."""
+"""Throughput when every frame takes the node-capacity overflow path (experiments)."""
 import sys
 from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
