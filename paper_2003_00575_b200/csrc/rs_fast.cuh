@@ -831,12 +831,12 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
     RS_MARK(7);
     // ---- X. cross-band unions over DSMEM -----------------------------------
     // Boundary edges are listed first (rows 1.. of the U plane are free now and
-    // serve as the buffer), then united by all threads in parallel.
-    if (r0 > 0) {
-        const int ku = k - 1;
-        const uint32_t *SBu = cl.map_shared_rank(SB, ku), *NBu = cl.map_shared_rank(NB, ku);
-        const uint32_t bandu = (uint32_t)ku << a.SHN;
-        const int wu0 = (R - 1) * WPR;
+    // serve as the buffer), then united by all threads in parallel.  The up
+    // edges across a boundary are listed by both bands next to it: the lower
+    // band takes the upper half of the words, the band above the lower half
+    // (reading the lower band's row-0 planes over DSMEM), so the boundary work
+    // is shared instead of falling on the lower band alone.
+    if (a.C > 1) {
         uint32_t *XL = U + WPR;
         const uint32_t xcap = (uint32_t)((rows - 1) * WPR / 2);
         // warp-aggregated: every lane calls, `has` lanes push an edge
@@ -855,32 +855,53 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
                 uf.unite(x, y);
             }
         };
-        for (int cbase = warp * 32; cbase < WPR * 32; cbase += kFastThreads) {
-            const int c = cbase + lane;
-            const int cw = c >> 5, b = c & 31;
-            const uint32_t uw = U[cw];
-            const uint32_t upb = b > 0 ? (uw >> (b - 1)) & 1u : (cw > 0 ? U[cw - 1] >> 31 : 0u);
-            const bool has = ((uw >> b) & 1u) && !(upb && ((L[cw] >> b) & 1u) && ((Lh[cw] >> b) & 1u));
-            xpush(has, has ? band | run_of(SB, NB, cw, b) : 0u, has ? bandu | run_of(SBu, NBu, wu0 + cw, b) : 0u);
-        }
-        for (int o = 0; o < a.n_off; ++o) {
-            const int dy = a.dy[o];
-            const uint32_t *M = MC + o * a.nwords, *T = TL + o * a.nwords;
-            for (int q = 0; q < min(dy, rows); ++q) {
-                const int tr = r0 + q - dy;
-                if (tr < 0) continue;
-                const int kt = tr / R, tq = tr - kt * R;
-                const uint32_t *SBt = cl.map_shared_rank(SB, kt), *NBt = cl.map_shared_rank(NB, kt);
-                for (int cbase = warp * 32; cbase < WPR * 32; cbase += kFastThreads) {
-                    const int c = cbase + lane;
-                    const int cw = c >> 5, b = c & 31, w = q * WPR + cw;
-                    const uint32_t m = M[w];
-                    const uint32_t mpb = b > 0 ? (m >> (b - 1)) & 1u : (cw > 0 ? M[w - 1] >> 31 : 0u);
-                    const bool has = c < W && ((m >> b) & 1u) && !(mpb && ((L[w] >> b) & 1u) && ((T[w] >> b) & 1u));
-                    int tc = (c - a.dx[o]) % W;
-                    if (tc < 0) tc += W;
-                    xpush(has, has ? band | run_of(SB, NB, w, b) : 0u,
-                          has ? ((uint32_t)kt << a.SHN) | run_of(SBt, NBt, tq * WPR + tc / 32, tc & 31) : 0u);
+        // up edges from row 0 of band bl to the last row of band bl - 1, words [wlo, whi)
+        auto boundary = [&](int bl, int wlo, int whi) {
+            const int bu = bl - 1;
+            const bool lower = bl == k;
+            const uint32_t *U0 = lower ? U : cl.map_shared_rank(U, bl);
+            const uint32_t *L0 = lower ? L : cl.map_shared_rank(L, bl);
+            const uint32_t *Lup = lower ? Lh : L + (R - 1) * WPR;   // left edges of the row above
+            const uint32_t *SBl = lower ? SB : cl.map_shared_rank(SB, bl);
+            const uint32_t *NBl = lower ? NB : cl.map_shared_rank(NB, bl);
+            const uint32_t *SBu = lower ? cl.map_shared_rank(SB, bu) : SB;
+            const uint32_t *NBu = lower ? cl.map_shared_rank(NB, bu) : NB;
+            const uint32_t tagl = (uint32_t)bl << a.SHN, tagu = (uint32_t)bu << a.SHN;
+            const int wu0 = (R - 1) * WPR;
+            for (int cbase = (wlo + warp) * 32; cbase < whi * 32; cbase += kFastThreads) {
+                const int c = cbase + lane;
+                const int cw = c >> 5, b = c & 31;
+                const uint32_t uw = U0[cw];
+                const uint32_t upb = b > 0 ? (uw >> (b - 1)) & 1u : (cw > 0 ? U0[cw - 1] >> 31 : 0u);
+                const bool has = ((uw >> b) & 1u) && !(upb && ((L0[cw] >> b) & 1u) && ((Lup[cw] >> b) & 1u));
+                xpush(has, has ? tagl | run_of(SBl, NBl, cw, b) : 0u,
+                      has ? tagu | run_of(SBu, NBu, wu0 + cw, b) : 0u);
+            }
+        };
+        const int whalf = WPR / 2;
+        if (r0 > 0) boundary(k, whalf, WPR);
+        if (k + 1 < a.C) boundary(k + 1, 0, whalf);
+        if (r0 > 0) {
+            for (int o = 0; o < a.n_off; ++o) {
+                const int dy = a.dy[o];
+                const uint32_t *M = MC + o * a.nwords, *T = TL + o * a.nwords;
+                for (int q = 0; q < min(dy, rows); ++q) {
+                    const int tr = r0 + q - dy;
+                    if (tr < 0) continue;
+                    const int kt = tr / R, tq = tr - kt * R;
+                    const uint32_t *SBt = cl.map_shared_rank(SB, kt), *NBt = cl.map_shared_rank(NB, kt);
+                    for (int cbase = warp * 32; cbase < WPR * 32; cbase += kFastThreads) {
+                        const int c = cbase + lane;
+                        const int cw = c >> 5, b = c & 31, w = q * WPR + cw;
+                        const uint32_t m = M[w];
+                        const uint32_t mpb = b > 0 ? (m >> (b - 1)) & 1u : (cw > 0 ? M[w - 1] >> 31 : 0u);
+                        const bool has =
+                            c < W && ((m >> b) & 1u) && !(mpb && ((L[w] >> b) & 1u) && ((T[w] >> b) & 1u));
+                        int tc = (c - a.dx[o]) % W;
+                        if (tc < 0) tc += W;
+                        xpush(has, has ? band | run_of(SB, NB, w, b) : 0u,
+                              has ? ((uint32_t)kt << a.SHN) | run_of(SBt, NBt, tq * WPR + tc / 32, tc & 31) : 0u);
+                    }
                 }
             }
         }

@@ -68,3 +68,11 @@ if okb.any():
     for nm, i, j in [("B.edges+seam", 1, 21), ("B.step-A MC", 21, 22), ("B.other MC", 22, 2)]:
         d3 = (buf[okb, j] - buf[okb, i]).astype(np.float64)
         print(f"  {nm:14s} mean {d3.mean():9.0f}  p90 {np.percentile(d3, 90):9.0f}")
+C = pipe.ctas_per_frame
+if C > 1:
+    rank = np.arange(n) % C
+    print("per band (CTA rank in the cluster): mean cycles of each phase")
+    print("  " + " ".join(f"{nm[:10]:>10s}" for nm in names))
+    for k in range(C):
+        m = rank == k
+        print(f"k={k} " + " ".join(f"{d[m, i].mean():10.0f}" for i in range(len(names))))
