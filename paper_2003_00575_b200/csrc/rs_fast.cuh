@@ -44,10 +44,14 @@ namespace rs {
 #ifndef RS_FAST_THREADS
 #define RS_FAST_THREADS 512
 #endif
+#ifndef RS_SWEEP_UNROLL
+#define RS_SWEEP_UNROLL 2   // cell-label sweep: iterations in flight per warp
+#endif
 #ifndef RS_STRIP_SETS
 #define RS_STRIP_SETS 4   // step A register sets: 4 = two-row prefetch, 3 = one-row prefetch
 #endif
 constexpr int kFastThreads = RS_FAST_THREADS;
+constexpr int kSweepUnroll = RS_SWEEP_UNROLL;
 constexpr int kFastOcc = RS_FAST_OCC;   // CTAs per SM the fast kernel is sized for
 constexpr int kFastWarps = kFastThreads / 32;
 
@@ -1046,7 +1050,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
         // index → address computation per load
         const uint32_t szb = smem_addr(SZ) - 4u;
         int4 *dst = reinterpret_cast<int4 *>(out) + warp * 32 + lane;
-#pragma unroll 2
+#pragma unroll kSweepUnroll
         for (int w0 = warp * 4; w0 < nw; w0 += kFastWarps * 4, dst += kFastWarps * 32) {
             const int w = w0 + (lane >> 3);
             const uint32_t pw = P[w] >> b0, sbw = SB[w];
