@@ -671,7 +671,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
                     k += __popc(m & ~(mprev & lw & TL[o * a.nwords + w]));
                 }
                 uint32_t slot = 0;
-                if (!direct) {
+                if (!direct && __any_sync(kFull, k != 0u)) {
                     // warp-aggregated reservation in the edge list
                     uint32_t inc = k;
                     for (int off = 1; off < 32; off <<= 1) {
@@ -797,14 +797,16 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
                 eb = P[w] & ~((L[w] >> 1) | (lnext << 31));
                 sb = SB[w];
             }
-            int inc = eb ? base + __ffs(eb) - 1 : INT_MAX;
-            for (int off = 1; off < 32; off <<= 1) {
-                const int t = __shfl_down_sync(kFull, inc, off);
-                if (lane + off < 32) inc = min(inc, t);
-            }
-            inc = min(inc, carry);
-            int exc = __shfl_down_sync(kFull, inc, 1);
-            if (lane == 31) exc = carry;
+            // first run end at or after this word (inc) and after it (exc):
+            // the first end of the next lane that has one (positions grow
+            // with the lane), else the carry from the chunk after this one
+            const int fe = eb ? base + __ffs(eb) - 1 : INT_MAX;
+            const uint32_t he = __ballot_sync(kFull, eb != 0u);
+            const uint32_t ge = he & ~((1u << lane) - 1u), gt = he & ~lanemask_le(lane);
+            const int li = ge ? __ffs(ge) - 1 : 0, lx = gt ? __ffs(gt) - 1 : 0;
+            const int fi = __shfl_sync(kFull, fe, li), fx = __shfl_sync(kFull, fe, lx);
+            const int inc = ge ? fi : carry;
+            const int exc = gt ? fx : carry;
             if (sb) {
                 uint32_t id = NB[w];
                 for (uint32_t m = sb; m; m &= m - 1, ++id) {
@@ -946,7 +948,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
         }
         const uint32_t m = __ballot_sync(kFull, kept);
         s = kept ? s : 0u;
-        for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(kFull, s, off);
+        s = __reduce_add_sync(kFull, s);
         if (lane == 0) {
             KB[base >> 5] = m;
             if (s) atomicAdd(&cta_sum, s);
