@@ -353,3 +353,25 @@ def test_natural_overflow_noise_frames(variant):
     for b in range(frames.shape[0]):
         k = int(want_n[b])
         assert np.array_equal(got_s[b, :k + 1], want_s[b, :k + 1])
+
+
+@pytest.mark.parametrize("cid,variant", [(1, "default"), (2, "core"), (4, "S1"), (3, "mc14_core")])
+def test_dense_kernel_when_fast_plan_impossible(cid, variant, config_frames):
+    """Band heights the fast kernel cannot hold (64 rows of 2048 cells, or more
+    rows than a 1024-wide frame needs) run rs_dense_kernel over the batch; the
+    results are the same as the oracle's."""
+    model = synthetic.sensor_for(synthetic.CONFIGS[cid])
+    pipe = rs.Pipeline(model, VARIANTS[variant], device="cuda:0", rows_per_cta=64)
+    if pipe.plan["fast"]:
+        pytest.skip("the fast plan holds this geometry")
+    frames = config_frames[cid][:4]
+    want_l, want_n, want_s = oracle.segment_batch(frames.cpu().numpy(), pipe.packed,
+                                                  sizes_stride=pipe.sizes_stride)
+    res = pipe.segment_batch(frames)
+    torch.cuda.synchronize()
+    assert np.array_equal(res.n_clusters.cpu().numpy(), want_n)
+    assert np.array_equal(res.labels.cpu().numpy(), want_l)
+    got_s = res.cluster_sizes.cpu().numpy()
+    for b in range(frames.shape[0]):
+        k = int(want_n[b])
+        assert np.array_equal(got_s[b, :k + 1], want_s[b, :k + 1])
