@@ -44,6 +44,9 @@ constexpr size_t kSmemLimit = 227 * 1024 - 4096;
 // static shared memory of each CTA
 constexpr size_t kFastSmemTarget = std::min<size_t>(228 * 1024 / rs::kFastOcc - 1024 - 2560, kSmemLimit);
 constexpr int kMinNodeCap = 512;
+#ifndef RS_UDYN_MIN_C
+#define RS_UDYN_MIN_C 2   // clusters of at least this many bands grab edges dynamically in the local unions
+#endif
 
 thread_local std::string g_err;
 
@@ -234,7 +237,7 @@ int make_plan(const rs_config *cfg, Plan *pl) {
             if (cfg->offsets[o][0] <= 2 && cfg->offsets[o][1] >= 0 && cfg->offsets[o][1] <= 31)
                 pl->kf.aoff[pl->kf.n_aoff++] = o;
         pl->kf.NC = (int)NC;
-        pl->kf.udyn = pl->kf.C >= 4;
+        pl->kf.udyn = pl->kf.C >= RS_UDYN_MIN_C;
         int SHN = 0;
         while ((1 << SHN) < NC) ++SHN;
         pl->kf.SHN = SHN;

@@ -37,7 +37,7 @@ struct KArgs {
     int NC, SHN;                  // fast kernel: run-node capacity per band, id bits
     int use_tma;                  // dense kernel: stage rows with TMA bulk copies
     int stop_after;               // experiments only: leave the fast kernel after phase N (0 = never)
-    int udyn;                     // fast kernel: dynamic edge grabbing in the local unions (clusters of >= 4 bands)
+    int udyn;                     // fast kernel: dynamic edge grabbing in the local unions (clusters of >= 2 bands)
     int n_aoff;                   // Map Connection offsets evaluated in step A (dy <= 2, 0 <= dx <= 31), at most 4
     int aoff[4];                  // their indices into dy/dx
 };
