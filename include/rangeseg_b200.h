@@ -34,10 +34,17 @@
  *   | two_cos_off[k][H] for k < n_offsets (indexed by the pair's upper row)
  * rs_tables_count(H, n_offsets) gives its length in floats.
  *
+ * Input contract (range_image.py:47-54, from_ranges): ranges finite and >= 0
+ * (0 = no return).  The kernels check it on the device as they read the
+ * ranges (no extra pass): a frame that breaks it gets n_clusters[b] =
+ * RS_FRAME_INVALID and undefined labels; rs_segment_batch_host turns that into
+ * RS_EINVAL (the reference's ValueError).
+ *
  * Output contract (bit-exact with the reference):
  *   labels[b][r][c]   int32, 0 = background (invalid, ground or filtered);
- *                     clusters numbered 1..K in first-encounter row-major order
- *   n_clusters[b]     K
+ *                     clusters numbered 1..K in first-encounter row-major order;
+ *                     the device buffer must be 16-byte aligned
+ *   n_clusters[b]     K (or RS_FRAME_INVALID, above)
  *   cluster_sizes[b][0..K]  int64 (optional, may be NULL); [0] = H*W - sum of
  *                     kept sizes; sizes_stride must be >= H*W/max(min,1) + 1
  */
@@ -52,6 +59,7 @@ extern "C" {
 #endif
 
 #define RS_MAX_OFFSETS 32
+#define RS_FRAME_INVALID (-1)   /* n_clusters[b] of a frame with a NaN, inf or negative range */
 
 enum rs_status {
     RS_OK = 0,
@@ -72,7 +80,8 @@ typedef struct rs_config {
     float keep_above;                       /* f32(GroundParams.resolve_keep_above) */
     float two_cos_h;                        /* f32(pair_constant(0, 1)) */
     int32_t rows_per_cta;                   /* 0 = automatic band height */
-    int32_t reserved[3];                    /* [0]: node-capacity cap (tests); else 0 */
+    int32_t reserved[3];                    /* [0]: node-capacity cap (tests, 0 = automatic);
+                                               [1], [2]: must be 0 (RS_EINVAL otherwise) */
 } rs_config;
 
 /* Number of floats in the constant-table block. */
@@ -87,20 +96,17 @@ int rs_plan(const rs_config *cfg, int32_t *rows_per_cta, int32_t *ctas_per_frame
  * fast smem, node capacity, dense rows, dense CTAs, dense smem}. */
 int rs_plan_detail(const rs_config *cfg, int32_t *out, int32_t n);
 
-/* Device workspace rs_segment_batch needs for `batch` frames: 0 bytes (the
- * path needs no scratch beyond the caller's buffers: a frame whose runs
- * exceed the node capacity is finished in its own label buffer).  Kept for
- * ABI stability; d_workspace / workspace_size may be NULL / 0. */
-size_t rs_workspace_size(const rs_config *cfg, int32_t batch);
-
 /* B frames, device pointers, enqueued on `stream` (a cudaStream_t; NULL = legacy
- * default stream).  One kernel launch; asynchronous: returns after it. */
+ * default stream).  One kernel launch; asynchronous: returns after it.  No
+ * workspace: a frame whose runs exceed the kernel's shared-memory node
+ * capacity is finished inside the same launch in its own label buffer. */
 int rs_segment_batch(const rs_config *cfg, const float *d_tables, const float *d_ranges,
                      int32_t batch, int32_t *d_labels, int32_t *d_n_clusters,
-                     int64_t *d_cluster_sizes, int64_t sizes_stride,
-                     void *d_workspace, size_t workspace_size, void *stream);
+                     int64_t *d_cluster_sizes, int64_t sizes_stride, void *stream);
 
-/* Same on host buffers (pinned memory gives overlapped copies).  Synchronous. */
+/* Same on host buffers (pinned memory gives overlapped copies).  Synchronous.
+ * Returns RS_EINVAL (after the copies) if a frame breaks the input contract;
+ * h_n_clusters may be NULL. */
 int rs_segment_batch_host(const rs_config *cfg, const float *h_tables, const float *h_ranges,
                           int32_t batch, int32_t *h_labels, int32_t *h_n_clusters,
                           int64_t *h_cluster_sizes, int64_t sizes_stride);
@@ -110,6 +116,18 @@ int rs_segment_batch_host(const rs_config *cfg, const float *h_tables, const flo
 int rs_stage_masks(const rs_config *cfg, const float *d_tables, const float *d_ranges,
                    int32_t batch, uint8_t *d_ground, uint8_t *d_horizontal,
                    uint8_t *d_vertical, void *stream);
+
+/* Parity export of the fused kernel's OWN edge decisions: rs_segment_batch
+ * (labels and counts as usual) that also writes the bit planes the kernel
+ * built after its edge step, uint32 words [B][3 + n_offsets][H][ceil(W/32)],
+ * bit c%32 of word c/32 for column c:
+ *   plane 0  presence: r > 0 and not ground     (= !extract_ground mask)
+ *   plane 1  left edge (r, c-1 mod W) - (r, c)   (= horizontal[r][c-1 mod W])
+ *   plane 2  up edge (r-1, c) - (r, c)           (= vertical[r-1][c]; row 0: 0)
+ *   plane 3+k  Map Connection k: (r-dy, c-dx mod W) - (r, c), rows r >= dy
+ * Only geometries the fast kernel runs (rs_plan_detail()[0] == 1). */
+int rs_fast_planes(const rs_config *cfg, const float *d_tables, const float *d_ranges, int32_t batch,
+                   uint32_t *d_planes, int32_t *d_labels, int32_t *d_n_clusters, void *stream);
 
 /* The stages on their own, with the reference's inputs (device buffers, B
  * frames, asynchronous on `stream`):

@@ -118,6 +118,22 @@ def segment_batch(ranges, packed, nthreads=None, sizes_stride=None):
     return labels, ncl, sizes
 
 
+def planes_batch(ranges, packed, nthreads=None):
+    """The edge decisions of [B,H,W] frames as packed bit planes, uint32
+    [B, 3 + n_offsets, H, ceil(W/32)] in rs_fast_planes' layout (presence,
+    left edge, up edge, one plane per Map Connection offset)."""
+    oc = OracleConfig(packed)
+    rg = np.ascontiguousarray(ranges, dtype=np.float32)
+    B = rg.shape[0]
+    H, W = packed.height, packed.width
+    planes = np.zeros((B, 3 + len(packed.offsets), H, (W + 31) // 32), dtype=np.uint32)
+    rc = lib().oracle_planes_batch(_ptr(rg, ctypes.c_float), B, ctypes.byref(oc.cfg),
+                                   _ptr(planes, ctypes.c_uint32), int(nthreads or os.cpu_count() or 1))
+    if rc != 0:
+        raise MemoryError("oracle allocation failed")
+    return planes
+
+
 class _ProjCfg(ctypes.Structure):
     _fields_ = [("height", ctypes.c_int32), ("width", ctypes.c_int32),
                 ("descending", ctypes.c_int32), ("azimuth_step", ctypes.c_double),

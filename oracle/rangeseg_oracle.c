@@ -301,3 +301,77 @@ int oracle_segment_batch(const float *ranges, int B, const oracle_cfg *cfg,
     }
     return failed ? -1 : 0;
 }
+
+/* ---- edge decisions as packed bit planes (parity of the fused kernel's own
+ * planes, rs_fast_planes in include/rangeseg_b200.h) ----------------------
+ * [3 + n_offsets][H][ceil(W/32)] uint32 per frame, bit c%32 of word c/32:
+ *   0 presence = valid and not ground          (ground.py:132-140, pipeline.py:109)
+ *   1 left edge (r,c-1 mod W)-(r,c) = horizontal[r][c-1 mod W]   (connectivity.py:80-84)
+ *   2 up edge (r-1,c)-(r,c) = vertical[r-1][c]                   (connectivity.py:86-90)
+ *   3+k Map Connection k: (r-dy, c-dx mod W)-(r,c) for r >= dy, both present and
+ *     pair_distance_sq <= d_max_sq with the pair's upper-row constant
+ *     (map_connections.py:155-169; the reference evaluates it only between
+ *     different labels, the plane holds the decision for every present pair). */
+static void oracle_frame_planes(const float *rg, const oracle_cfg *cfg, uint32_t *out,
+                                uint8_t *gm, uint8_t *hz, uint8_t *vt) {
+    const int H = cfg->height, W = cfg->width, WPR = (W + 31) / 32;
+    const size_t fw = (size_t)H * WPR;
+    oracle_ground(rg, cfg, gm);
+    oracle_connectivity(rg, gm, cfg, hz, vt);
+    memset(out, 0, sizeof(uint32_t) * fw * (size_t)(3 + cfg->n_offsets));
+#define SETB(pl, r, c) out[(size_t)(pl) * fw + (size_t)(r) * WPR + ((c) >> 5)] |= 1u << ((c) & 31)
+#define PRES(r, c) (rg[(r) * W + (c)] > 0.0f && !gm[(r) * W + (c)])
+    for (int r = 0; r < H; ++r)
+        for (int c = 0; c < W; ++c) {
+            if (PRES(r, c)) SETB(0, r, c);
+            if (W > 1 && hz[r * W + (c + W - 1) % W]) SETB(1, r, c);
+            if (r >= 1 && vt[(r - 1) * W + c]) SETB(2, r, c);
+        }
+    for (int k = 0; k < cfg->n_offsets; ++k) {
+        const int dy = cfg->offsets[2 * k], dx = cfg->offsets[2 * k + 1];
+        const float *tc = cfg->tables + H + 5 * (H - 1) + (size_t)k * H;
+        for (int r = dy; r < H; ++r)
+            for (int c = 0; c < W; ++c) {
+                const int ur = r - dy, uc = ((c - dx) % W + W) % W;
+                if (PRES(r, c) && PRES(ur, uc) && pair_ok(rg[ur * W + uc], rg[r * W + c], tc[ur], cfg->d_max_sq))
+                    SETB(3 + k, r, c);
+            }
+    }
+#undef SETB
+#undef PRES
+}
+
+typedef struct {
+    const float *ranges; const oracle_cfg *cfg; uint32_t *planes; int B, tid, nthreads; int failed;
+} planes_job;
+
+static void *planes_worker(void *arg) {
+    planes_job *j = (planes_job *)arg;
+    const int H = j->cfg->height, W = j->cfg->width, WPR = (W + 31) / 32;
+    const size_t HW = (size_t)H * W, pw = (size_t)(3 + j->cfg->n_offsets) * H * WPR;
+    uint8_t *gm = malloc(HW), *hz = malloc(HW), *vt = malloc(HW);
+    if (!gm || !hz || !vt) { j->failed = 1; free(gm); free(hz); free(vt); return NULL; }
+    for (int f = j->tid; f < j->B; f += j->nthreads)
+        oracle_frame_planes(j->ranges + f * HW, j->cfg, j->planes + f * pw, gm, hz, vt);
+    free(gm); free(hz); free(vt);
+    return NULL;
+}
+
+int oracle_planes_batch(const float *ranges, int B, const oracle_cfg *cfg, uint32_t *planes, int nthreads) {
+    if (nthreads < 1) nthreads = 1;
+    if (nthreads > B) nthreads = B > 0 ? B : 1;
+    if (nthreads > 256) nthreads = 256;
+    pthread_t th[256];
+    planes_job jobs[256];
+    for (int t = 0; t < nthreads; ++t) {
+        jobs[t] = (planes_job){ranges, cfg, planes, B, t, nthreads, 0};
+        if (nthreads == 1) planes_worker(&jobs[0]);
+        else pthread_create(&th[t], NULL, planes_worker, &jobs[t]);
+    }
+    int failed = 0;
+    for (int t = 0; t < nthreads; ++t) {
+        if (nthreads > 1) pthread_join(th[t], NULL);
+        failed |= jobs[t].failed;
+    }
+    return failed ? -1 : 0;
+}

@@ -16,9 +16,10 @@ LIB_PATH = Path(os.environ.get("RS_LIB") or
 MAX_OFFSETS = 32
 
 RS_OK, RS_EINVAL, RS_ECUDA, RS_ETOOLARGE, RS_ENODEV = range(5)
+RS_FRAME_INVALID = -1   # n_clusters[b] of a frame that breaks the input contract
 
-EXPORTS = ("rs_tables_count", "rs_plan", "rs_plan_detail", "rs_workspace_size",
-           "rs_segment_batch", "rs_segment_batch_host", "rs_stage_masks", "rs_project",
+EXPORTS = ("rs_tables_count", "rs_plan", "rs_plan_detail",
+           "rs_segment_batch", "rs_segment_batch_host", "rs_fast_planes", "rs_stage_masks", "rs_project",
            "rs_project_workspace_size", "rs_contingency", "rs_contingency_workspace_size",
            "rs_height_image", "rs_ground_mask", "rs_connectivity",
            "rs_labels_to_points", "rs_phase_profile", "rs_last_error", "rs_version")
@@ -64,12 +65,12 @@ def lib():
                               ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_size_t)]
         L.rs_segment_batch.restype = ctypes.c_int
         L.rs_segment_batch.argtypes = [ctypes.POINTER(RsConfig), _P, _P, ctypes.c_int32,
-                                       _P, _P, _P, ctypes.c_int64, _P, ctypes.c_size_t, _P]
+                                       _P, _P, _P, ctypes.c_int64, _P]
+        L.rs_fast_planes.restype = ctypes.c_int
+        L.rs_fast_planes.argtypes = [ctypes.POINTER(RsConfig), _P, _P, ctypes.c_int32, _P, _P, _P, _P]
         L.rs_plan_detail.restype = ctypes.c_int
         L.rs_plan_detail.argtypes = [ctypes.POINTER(RsConfig), ctypes.POINTER(ctypes.c_int32),
                                      ctypes.c_int32]
-        L.rs_workspace_size.restype = ctypes.c_size_t
-        L.rs_workspace_size.argtypes = [ctypes.POINTER(RsConfig), ctypes.c_int32]
         L.rs_segment_batch_host.restype = ctypes.c_int
         L.rs_segment_batch_host.argtypes = [ctypes.POINTER(RsConfig), _P, _P, ctypes.c_int32,
                                             _P, _P, _P, ctypes.c_int64]
@@ -130,7 +131,7 @@ def make_config(packed, rows_per_cta: int = 0, node_capacity: int = 0,
     cfg.two_cos_h = float(packed.two_cos_h)
     cfg.rows_per_cta = int(rows_per_cta)
     cfg.reserved[0] = int(node_capacity)
-    cfg.reserved[1] = int(stop_after)   # experiments only: truncated kernel, wrong labels
+    cfg.reserved[1] = int(stop_after)   # RS_EXPERIMENTS builds only (else RS_EINVAL): truncated kernel
     return cfg
 
 

@@ -38,6 +38,19 @@ def project_config(model: SensorModel):
     return pc, asc
 
 
+def _launch_stream(dev, stream, tensors):
+    """The stream a launch goes on: ``stream`` (made to wait for the current
+    stream's queued work, its tensors recorded on it so the caching allocator
+    does not reuse them early) or the current stream."""
+    cur = torch.cuda.current_stream(dev)
+    if stream is None or stream.cuda_stream == cur.cuda_stream:
+        return cur
+    stream.wait_stream(cur)
+    for t in tensors:
+        t.record_stream(stream)
+    return stream
+
+
 def _check_points(points) -> np.ndarray:
     pts = np.asarray(points, dtype=np.float64)
     if pts.ndim != 2 or pts.shape[1] < 3 or pts.shape[0] == 0:
@@ -58,21 +71,22 @@ def project_batch(points: torch.Tensor, offsets: torch.Tensor, model: SensorMode
         raise ValueError("points must be a float64 CUDA tensor [N, >=3]")
     if offsets.dtype != torch.int64 or offsets.dim() != 1 or offsets.device != points.device:
         raise ValueError("offsets must be an int64 tensor [B+1] on the points' device")
-    points = points.contiguous()
     pc, asc = project_config(model)
     dev = points.device
     B = offsets.numel() - 1
     H, W = model.height, model.width
-    d_asc = torch.from_numpy(asc).to(dev)
-    ranges = torch.empty((B, H, W), dtype=torch.float32, device=dev)
-    pidx = torch.empty((B, H, W), dtype=torch.int64, device=dev)
-    counts = torch.empty((B, 2), dtype=torch.int64, device=dev)
-    wsb = int(_native.lib().rs_project_workspace_size(points.shape[0]))
-    ws = torch.empty((max(wsb, 4),), dtype=torch.uint8, device=dev)
-    s = stream if stream is not None else torch.cuda.current_stream(dev)
-    st = _native.lib().rs_project(ctypes.byref(pc), _ptr(d_asc), _ptr(points), points.shape[1],
-                                  _ptr(offsets), B, points.shape[0], _ptr(ranges), _ptr(pidx),
-                                  _ptr(counts), _ptr(ws), wsb, ctypes.c_void_p(s.cuda_stream))
+    with torch.cuda.device(dev):
+        points = points.contiguous()
+        d_asc = torch.from_numpy(asc).to(dev)
+        ranges = torch.empty((B, H, W), dtype=torch.float32, device=dev)
+        pidx = torch.empty((B, H, W), dtype=torch.int64, device=dev)
+        counts = torch.empty((B, 2), dtype=torch.int64, device=dev)
+        wsb = int(_native.lib().rs_project_workspace_size(points.shape[0]))
+        ws = torch.empty((max(wsb, 4),), dtype=torch.uint8, device=dev)
+        s = _launch_stream(dev, stream, (points, offsets, d_asc, ranges, pidx, counts, ws))
+        st = _native.lib().rs_project(ctypes.byref(pc), _ptr(d_asc), _ptr(points), points.shape[1],
+                                      _ptr(offsets), B, points.shape[0], _ptr(ranges), _ptr(pidx),
+                                      _ptr(counts), _ptr(ws), wsb, ctypes.c_void_p(s.cuda_stream))
     _native.check(st, "rs_project")
     return ranges, pidx, counts
 
@@ -81,12 +95,21 @@ def labels_to_points_batch(labels: torch.Tensor, point_index: torch.Tensor, offs
                            stream: torch.cuda.Stream | None = None) -> torch.Tensor:
     """Device labels [B,H,W] -> per-point int32 labels [N] (0 = dropped / lost a cell)."""
     B, H, W = labels.shape
+    if labels.dtype != torch.int32 or point_index.dtype != torch.int64 or offsets.dtype != torch.int64:
+        raise ValueError("labels int32, point_index int64 and offsets int64 expected")
+    if tuple(point_index.shape) != (B, H, W) or offsets.shape != (B + 1,):
+        raise ValueError("point_index must be [B, H, W] and offsets [B + 1] like labels")
+    dev = labels.device
+    if point_index.device != dev or offsets.device != dev:
+        raise ValueError("labels, point_index and offsets must be on one device")
     n = int(offsets[-1].item())
-    out = torch.empty((n,), dtype=torch.int32, device=labels.device)
-    s = stream if stream is not None else torch.cuda.current_stream(labels.device)
-    st = _native.lib().rs_labels_to_points(_ptr(labels.contiguous()), _ptr(point_index.contiguous()),
-                                           _ptr(offsets), B, H, W, n, _ptr(out),
-                                           ctypes.c_void_p(s.cuda_stream))
+    with torch.cuda.device(dev):
+        labels, point_index = labels.contiguous(), point_index.contiguous()
+        out = torch.empty((n,), dtype=torch.int32, device=dev)
+        s = _launch_stream(dev, stream, (labels, point_index, offsets, out))
+        st = _native.lib().rs_labels_to_points(_ptr(labels), _ptr(point_index),
+                                               _ptr(offsets), B, H, W, n, _ptr(out),
+                                               ctypes.c_void_p(s.cuda_stream))
     _native.check(st, "rs_labels_to_points")
     return out
 

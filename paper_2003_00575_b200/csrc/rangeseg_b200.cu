@@ -78,6 +78,10 @@ int validate(const rs_config *cfg) {
     }
     if (cfg->rows_per_cta < 0 || cfg->rows_per_cta > kMaxRowsFast)
         return fail(RS_EINVAL, "rows_per_cta must be in [0, 64]");
+    if (cfg->reserved[0] < 0) return fail(RS_EINVAL, "reserved[0] (node capacity) must be >= 0");
+#ifndef RS_EXPERIMENTS
+    if (cfg->reserved[1] != 0 || cfg->reserved[2] != 0) return fail(RS_EINVAL, "reserved[1] and reserved[2] must be 0");
+#endif
     return RS_OK;
 }
 
@@ -161,6 +165,7 @@ int max_runs(int R, int W) { return R * W + rs::kFastWarps; }
 struct Plan {
     bool fast;            // run rs_fast_kernel (else rs_dense_kernel directly)
     bool may_overflow;    // a band may exceed the node capacity (fast kernel's overflow path, rs_overflow.cuh)
+    bool dense_ok;        // rs_dense_kernel can hold the geometry
     KArgs kf, kd;         // arguments of the fast / dense kernels
     size_t smem_f, smem_d;
     int stop_after;       // experiments (rs_config.reserved[1]); 0 in production
@@ -176,29 +181,35 @@ int pick_dense_rows(const rs_config *cfg) {
     return std::min(R, H);
 }
 
-int make_plan(const rs_config *cfg, Plan *pl) {
+int make_plan_uncached(const rs_config *cfg, Plan *pl) {
     int st = validate(cfg);
     if (st) return st;
     const int H = cfg->height, W = cfg->width, n_off = cfg->n_offsets;
+#ifdef RS_EXPERIMENTS
     pl->stop_after = cfg->reserved[1];
+#else
+    pl->stop_after = 0;
+#endif
 
-    // dense plan (fallback / overflow path)
+    // dense plan (geometries the fast plan cannot hold)
     int Rd = cfg->rows_per_cta > 0 ? std::min({cfg->rows_per_cta, H, kMaxRowsPerCta}) : pick_dense_rows(cfg);
     if (dense_layout(Rd, W, n_off, nullptr) > kSmemLimit) Rd = pick_dense_rows(cfg);
     const int Cd = (H + Rd - 1) / Rd;
     const size_t smem_d = dense_layout(Rd, W, n_off, nullptr);
+    std::string dense_err;
     if (Cd > kMaxCluster)
-        return fail(RS_ETOOLARGE, "frame needs " + std::to_string(Cd) + " bands of " + std::to_string(Rd) +
-                                      " rows; a cluster holds at most 16");
-    if (smem_d > kSmemLimit)
-        return fail(RS_ETOOLARGE, "band of " + std::to_string(Rd) + "x" + std::to_string(W) + " cells needs " +
-                                      std::to_string(smem_d) + " B of shared memory");
+        dense_err = "frame needs " + std::to_string(Cd) + " bands of " + std::to_string(Rd) +
+                    " rows; a cluster holds at most 16";
+    else if (smem_d > kSmemLimit)
+        dense_err = "band of " + std::to_string(Rd) + "x" + std::to_string(W) + " cells needs " +
+                    std::to_string(smem_d) + " B of shared memory";
     fill_common(cfg, Rd, pl->kd);
     dense_layout(Rd, W, n_off, &pl->kd);
     int SH = 0;
     while ((1 << SH) < Rd * W) ++SH;
     pl->kd.SH = SH;
     pl->smem_d = smem_d;
+    pl->dense_ok = dense_err.empty();
 
     // fast plan: ~16K cells per band, node capacity from the shared-memory target
     // ~64K cells per band: fewer, larger bands mean fewer cross-band edges and
@@ -246,7 +257,36 @@ int make_plan(const rs_config *cfg, Plan *pl) {
         pl->may_overflow = NC < cap_full;
         break;
     }
+    if (!pl->fast && !pl->dense_ok) return fail(RS_ETOOLARGE, dense_err);
     return RS_OK;
+}
+
+// Plans are cached per thread: a Pipeline calls with the same config every
+// time, and planning (a capacity search per band height) costs microseconds.
+struct PlanCache {
+    bool valid = false;
+    rs_config cfg;
+    Plan pl;
+    int st = RS_OK;
+    std::string err;
+};
+thread_local PlanCache g_plan_cache;
+
+int make_plan(const rs_config *cfg, Plan *pl) {
+    if (!cfg) return fail(RS_EINVAL, "config is NULL");
+    PlanCache &c = g_plan_cache;
+    if (c.valid && memcmp(&c.cfg, cfg, sizeof(rs_config)) == 0) {
+        if (c.st) return fail(c.st, c.err);
+        *pl = c.pl;
+        return RS_OK;
+    }
+    const int st = make_plan_uncached(cfg, pl);
+    c.cfg = *cfg;
+    c.st = st;
+    c.err = st ? g_err : std::string();
+    if (!st) c.pl = *pl;
+    c.valid = true;
+    return st;
 }
 
 std::mutex g_attr_mu;
@@ -311,7 +351,8 @@ int launch_cluster(Kern kern, const KArgs &k, int clusters, int threads, size_t 
 // capacity are finished by the same kernel, rs_overflow.cuh), or
 // rs_dense_kernel when the fast plan cannot hold the geometry.
 int segment_launch(const Plan &pl, const float *d_tables, const float *d_ranges, int32_t batch, int32_t *d_labels,
-                   int32_t *d_n_clusters, int64_t *d_cluster_sizes, int64_t sizes_stride, cudaStream_t stream) {
+                   int32_t *d_n_clusters, int64_t *d_cluster_sizes, int64_t sizes_stride, cudaStream_t stream,
+                   uint32_t *d_planes = nullptr) {
     int st = set_attrs(pl);
     if (st) return st;
     KArgs k = pl.fast ? pl.kf : pl.kd;
@@ -327,15 +368,27 @@ int segment_launch(const Plan &pl, const float *d_tables, const float *d_ranges,
                               "rs_dense_kernel launch");
     }
     k.stop_after = pl.stop_after;
+    k.planes = d_planes;
     return k.n_aoff > 0 ? launch_cluster(rs::rs_fast_kernel<true>, k, batch, rs::kFastThreads, pl.smem_f, stream,
                                          "rs_fast_kernel launch")
                         : launch_cluster(rs::rs_fast_kernel<false>, k, batch, rs::kFastThreads, pl.smem_f, stream,
                                          "rs_fast_kernel launch");
 }
 
-// No device workspace is needed any more (the overflow path works in the label
-// buffer); the ABI keeps the workspace arguments, which are ignored.
-size_t workspace_bytes(int32_t) { return 0; }
+// Output checks shared by the device and host entries (before any allocation
+// or launch): the sizes stride bounds the label values the kernels write.
+int validate_outputs(const rs_config *cfg, int32_t batch, const void *labels, const void *sizes,
+                     int64_t sizes_stride) {
+    if (batch < 0) return fail(RS_EINVAL, "batch must be >= 0");
+    if (batch > 0 && !labels) return fail(RS_EINVAL, "labels are required");
+    if (sizes) {
+        const long long need = (long long)cfg->height * cfg->width / std::max(cfg->min_cluster_points, 1) + 1;
+        if (sizes_stride < need)
+            return fail(RS_EINVAL, "sizes_stride must be >= H*W/max(min_cluster_points,1)+1 = " +
+                                       std::to_string(need));
+    }
+    return RS_OK;
+}
 
 }  // namespace
 
@@ -346,12 +399,6 @@ extern "C" {
 size_t rs_tables_count(int32_t height, int32_t n_offsets) {
     if (height < 2 || n_offsets < 0) return 0;
     return (size_t)height + 5u * (size_t)(height - 1) + (size_t)n_offsets * height;
-}
-
-size_t rs_workspace_size(const rs_config *cfg, int32_t batch) {
-    Plan pl;
-    if (make_plan(cfg, &pl)) return 0;
-    return workspace_bytes(batch);
 }
 
 int rs_plan(const rs_config *cfg, int32_t *rows_per_cta, int32_t *ctas_per_frame, size_t *smem_bytes) {
@@ -377,36 +424,43 @@ int rs_plan_detail(const rs_config *cfg, int32_t *out, int32_t n) {
 
 int rs_segment_batch(const rs_config *cfg, const float *d_tables, const float *d_ranges, int32_t batch,
                      int32_t *d_labels, int32_t *d_n_clusters, int64_t *d_cluster_sizes, int64_t sizes_stride,
-                     void *d_workspace, size_t workspace_size, void *stream) {
+                     void *stream) {
     Plan pl;
     int st = make_plan(cfg, &pl);
     if (st) return st;
-    if (batch < 0) return fail(RS_EINVAL, "batch must be >= 0");
+    if ((st = validate_outputs(cfg, batch, d_labels, d_cluster_sizes, sizes_stride))) return st;
     if (batch == 0) return RS_OK;
-    if (!d_tables || !d_ranges || !d_labels) return fail(RS_EINVAL, "tables, ranges and labels are required");
-    const long long HW = (long long)cfg->height * cfg->width;
-    if (d_cluster_sizes) {
-        const long long need = HW / std::max(cfg->min_cluster_points, 1) + 1;
-        if (sizes_stride < need)
-            return fail(RS_EINVAL, "sizes_stride must be >= H*W/max(min_cluster_points,1)+1 = " +
-                                       std::to_string(need));
-    }
+    if (!d_tables || !d_ranges) return fail(RS_EINVAL, "tables and ranges are required");
+    if (reinterpret_cast<uintptr_t>(d_labels) & 15u) return fail(RS_EINVAL, "d_labels must be 16-byte aligned");
     if ((long long)batch * std::max(pl.kf.C, pl.kd.C) > 0x7fffffffLL) return fail(RS_EINVAL, "batch too large");
-    (void)d_workspace;
-    (void)workspace_size;
     return segment_launch(pl, d_tables, d_ranges, batch, d_labels, d_n_clusters, d_cluster_sizes, sizes_stride,
                           static_cast<cudaStream_t>(stream));
 }
 
-int rs_stage_masks(const rs_config *cfg, const float *d_tables, const float *d_ranges, int32_t batch,
-                   uint8_t *d_ground, uint8_t *d_horizontal, uint8_t *d_vertical, void *stream) {
+int rs_fast_planes(const rs_config *cfg, const float *d_tables, const float *d_ranges, int32_t batch,
+                   uint32_t *d_planes, int32_t *d_labels, int32_t *d_n_clusters, void *stream) {
     Plan pl;
     int st = make_plan(cfg, &pl);
+    if (st) return st;
+    if ((st = validate_outputs(cfg, batch, d_labels, nullptr, 0))) return st;
+    if (!pl.fast) return fail(RS_EINVAL, "the fast kernel does not run this geometry (no planes to export)");
+    if (batch == 0) return RS_OK;
+    if (!d_tables || !d_ranges || !d_planes) return fail(RS_EINVAL, "tables, ranges and planes are required");
+    if (reinterpret_cast<uintptr_t>(d_labels) & 15u) return fail(RS_EINVAL, "d_labels must be 16-byte aligned");
+    if ((long long)batch * pl.kf.C > 0x7fffffffLL) return fail(RS_EINVAL, "batch too large");
+    return segment_launch(pl, d_tables, d_ranges, batch, d_labels, d_n_clusters, nullptr, 0,
+                          static_cast<cudaStream_t>(stream), d_planes);
+}
+
+int rs_stage_masks(const rs_config *cfg, const float *d_tables, const float *d_ranges, int32_t batch,
+                   uint8_t *d_ground, uint8_t *d_horizontal, uint8_t *d_vertical, void *stream) {
+    int st = validate(cfg);
     if (st) return st;
     if (batch <= 0) return batch == 0 ? RS_OK : fail(RS_EINVAL, "batch must be >= 0");
     if (!d_tables || !d_ranges || !d_ground || !d_horizontal || !d_vertical)
         return fail(RS_EINVAL, "all buffers are required");
-    KArgs k = pl.kd;
+    KArgs k;
+    fill_common(cfg, 1, k);
     k.ranges = d_ranges;
     k.tables = d_tables;
     const long long total = (long long)batch * cfg->height * cfg->width;
@@ -419,12 +473,11 @@ int rs_stage_masks(const rs_config *cfg, const float *d_tables, const float *d_r
 namespace {
 int stage_launch_args(const rs_config *cfg, const float *d_tables, const float *d_ranges, int32_t batch, KArgs &k,
                       long long &total, int &blocks) {
-    Plan pl;
-    int st = make_plan(cfg, &pl);
+    int st = validate(cfg);
     if (st) return st;
     if (batch < 0) return fail(RS_EINVAL, "batch must be >= 0");
     if (batch > 0 && (!d_tables || !d_ranges)) return fail(RS_EINVAL, "tables and ranges are required");
-    k = pl.kd;
+    fill_common(cfg, 1, k);
     k.ranges = d_ranges;
     k.tables = d_tables;
     total = (long long)batch * cfg->height * cfg->width;
@@ -478,6 +531,7 @@ struct HostCtx {
     std::mutex mu;
     float *d_ranges = nullptr, *d_tables = nullptr;
     int32_t *d_labels = nullptr, *d_ncl = nullptr;
+    int32_t *h_ncl = nullptr;   // pinned: cluster counts when the caller passes none (invalid-frame check)
     int64_t *d_sizes = nullptr;
     // kHostStreams streams round-robin over chunks, so the host->device copy
     // of chunk j+2 can run while chunk j is copied back (both copy engines busy)
@@ -493,6 +547,8 @@ void host_free() {
     cudaFree(g_host.d_labels);
     cudaFree(g_host.d_ncl);
     cudaFree(g_host.d_sizes);
+    cudaFreeHost(g_host.h_ncl);
+    g_host.h_ncl = nullptr;
     g_host.d_ranges = nullptr;
     g_host.d_labels = nullptr;
     g_host.d_ncl = nullptr;
@@ -508,9 +564,10 @@ int rs_segment_batch_host(const rs_config *cfg, const float *h_tables, const flo
     Plan pl;
     int st = make_plan(cfg, &pl);
     if (st) return st;
-    if (batch < 0) return fail(RS_EINVAL, "batch must be >= 0");
+    if ((st = validate_outputs(cfg, batch, h_labels, h_cluster_sizes, sizes_stride))) return st;
     if (batch == 0) return RS_OK;
-    if (!h_tables || !h_ranges || !h_labels) return fail(RS_EINVAL, "tables, ranges and labels are required");
+    if (!h_tables || !h_ranges) return fail(RS_EINVAL, "tables and ranges are required");
+    if ((long long)batch * std::max(pl.kf.C, pl.kd.C) > 0x7fffffffLL) return fail(RS_EINVAL, "batch too large");
     std::lock_guard<std::mutex> g(g_host.mu);
     int dev = 0;
     if ((st = cuda_check(cudaGetDevice(&dev), "cudaGetDevice"))) return st;
@@ -534,7 +591,8 @@ int rs_segment_batch_host(const rs_config *cfg, const float *h_tables, const flo
         g_host.frame_cells = HW;
         if ((st = cuda_check(cudaMalloc(&g_host.d_ranges, (size_t)batch * HW * 4), "cudaMalloc ranges")) ||
             (st = cuda_check(cudaMalloc(&g_host.d_labels, (size_t)batch * HW * 4), "cudaMalloc labels")) ||
-            (st = cuda_check(cudaMalloc(&g_host.d_ncl, (size_t)batch * 4), "cudaMalloc n_clusters")))
+            (st = cuda_check(cudaMalloc(&g_host.d_ncl, (size_t)batch * 4), "cudaMalloc n_clusters")) ||
+            (st = cuda_check(cudaMallocHost(&g_host.h_ncl, (size_t)batch * 4), "cudaMallocHost n_clusters")))
             return st;
         if (h_cluster_sizes &&
             (st = cuda_check(cudaMalloc(&g_host.d_sizes, (size_t)batch * sizes_stride * 8), "cudaMalloc sizes")))
@@ -569,8 +627,8 @@ int rs_segment_batch_host(const rs_config *cfg, const float *h_tables, const flo
         if ((st = cuda_check(cudaMemcpyAsync(h_labels + off, g_host.d_labels + off, nb * HW * 4,
                                              cudaMemcpyDeviceToHost, s), "copy labels")))
             break;
-        if (h_n_clusters &&
-            (st = cuda_check(cudaMemcpyAsync(h_n_clusters + b0, g_host.d_ncl + b0, nb * 4, cudaMemcpyDeviceToHost, s),
+        int32_t *ncl_dst = h_n_clusters ? h_n_clusters : g_host.h_ncl;
+        if ((st = cuda_check(cudaMemcpyAsync(ncl_dst + b0, g_host.d_ncl + b0, nb * 4, cudaMemcpyDeviceToHost, s),
                              "copy n_clusters")))
             break;
         if (h_cluster_sizes &&
@@ -586,7 +644,12 @@ int rs_segment_batch_host(const rs_config *cfg, const float *h_tables, const flo
         if (!sst) sst = e;
     }
     cudaEventDestroy(tables_ready);
-    return st ? st : sst;
+    if (st || sst) return st ? st : sst;
+    const int32_t *ncl = h_n_clusters ? h_n_clusters : g_host.h_ncl;
+    for (int b = 0; b < batch; ++b)
+        if (ncl[b] == RS_FRAME_INVALID)
+            return fail(RS_EINVAL, "frame " + std::to_string(b) + ": ranges must be finite and >= 0");
+    return RS_OK;
 }
 
 int rs_project(const rs_project_config *pc, const double *d_asc, const double *d_points, int32_t stride,
@@ -734,6 +797,6 @@ int rs_phase_profile(int64_t *host_out, int32_t max_ctas) {
 
 const char *rs_last_error(void) { return g_err.c_str(); }
 
-int rs_version(void) { return 201; }
+int rs_version(void) { return 300; }
 
 }  // extern "C"

@@ -36,7 +36,8 @@ struct KArgs {
     int o_P, o_L, o_U, o_SB, o_RS, o_Ph, o_Lh, o_MC, o_TL, o_LR, o_K, o_E, o_SZ;
     int NC, SHN;                  // fast kernel: run-node capacity per band, id bits
     int use_tma;                  // dense kernel: stage rows with TMA bulk copies
-    int stop_after;               // experiments only: leave the fast kernel after phase N (0 = never)
+    int stop_after;               // experiments only (RS_EXPERIMENTS builds): leave the fast kernel after phase N
+    uint32_t *planes;             // debug export (rs_fast_planes): the fast kernel's bit planes after step B, or NULL
     int udyn;                     // fast kernel: dynamic edge grabbing in the local unions (clusters of >= 2 bands)
     int n_aoff;                   // Map Connection offsets evaluated in step A (dy <= 2, 0 <= dx <= 31), at most 4
     int aoff[4];                  // their indices into dy/dx
@@ -187,6 +188,15 @@ __device__ __forceinline__ bool present_at(const KArgs &a, int r, int c, Get get
     const int kk = (r >= 1 ? r : 1) - 1;
     return !ground_rule(a, ground_row(a, r), get(kk, c), get(kk + 1, c), v);
 }
+
+// Input contract of from_ranges (range_image.py:47-54): finite and >= 0
+// (-0.0 passes: it is not < 0).
+__device__ __forceinline__ bool range_ok(float v) { return v >= 0.f && v <= 3.4028234663852886e38f; }
+
+// Fast screen for the contract: the unsigned maximum of the raw bits of the
+// ranges seen exceeds FLT_MAX's bits iff some value is +inf, NaN or has its
+// sign bit set (a violation, or -0.0, which passes: range_ok re-checks).
+constexpr uint32_t kMaxFiniteBits = 0x7f7fffffu;
 
 __device__ __forceinline__ int divWPR(const KArgs &a, int w) {
     return (int)(((unsigned long long)(unsigned)w * a.magicWPR) >> 40);

@@ -96,6 +96,7 @@ struct DenseUF {
 struct DenseShared {
     uint32_t warp_tot[kDenseWarps];
     uint32_t cta_cnt, cta_sum, cta_prefix, seam;
+    uint32_t bad;   // a range of the band breaks the input contract (range_image.py:50-53)
 };
 
 __device__ __forceinline__ void dense_frame(const KArgs &a, uint32_t *sm, DenseShared &sh, uint64_t *mbar,
@@ -126,7 +127,10 @@ __device__ __forceinline__ void dense_frame(const KArgs &a, uint32_t *sm, DenseS
     // ---- 1. stage rows [lo_row, hi_row] (TMA bulk copies) ---------------------
     const int n_stage = (hi_row - lo_row + 1) * W;
     const float *src = fr + (size_t)lo_row * W;
-    if (tid == 0) seam = 0;
+    if (tid == 0) {
+        seam = 0;
+        sh.bad = 0;
+    }
     if (a.use_tma) {
         if (tid == 0) {
             mbar_expect_tx(mbar, (uint32_t)n_stage * 4u);
@@ -151,6 +155,7 @@ __device__ __forceinline__ void dense_frame(const KArgs &a, uint32_t *sm, DenseS
     {
         const float *tcv = a.tables + 5 * H - 4;
         const int rstart = r0 > 0 ? r0 - 1 : 0;
+        bool bad = false;
         for (int cw = warp; cw < WPR; cw += kDenseWarps) {
             const int c = cw * 32 + lane;
             const bool inb = c < W;
@@ -158,6 +163,7 @@ __device__ __forceinline__ void dense_frame(const KArgs &a, uint32_t *sm, DenseS
             bool pprev = false;
             for (int r = rstart; r < r0 + rows; ++r) {
                 const float v = inb ? S(r, c) : 0.f;
+                bad |= !range_ok(v);
                 bool p = v > 0.f;
                 if (a.ground && p) {
                     const float d1 = r >= 1 ? vprev : v;
@@ -186,6 +192,7 @@ __device__ __forceinline__ void dense_frame(const KArgs &a, uint32_t *sm, DenseS
                 pprev = p;
             }
         }
+        if (__any_sync(kFull, bad) && lane == 0) sh.bad = 1u;
     }
     __syncthreads();
 
@@ -512,16 +519,17 @@ __device__ __forceinline__ void dense_frame(const KArgs &a, uint32_t *sm, DenseS
     cl.sync();   // #5: every band's kept count and kept-size sum are published
     RS_MARK(10);
     if (tid == 0) {
-        uint32_t pre = 0, tot = 0, sum = 0;
+        uint32_t pre = 0, tot = 0, sum = 0, bad = 0;
         for (int j = 0; j < a.C; ++j) {
             const uint32_t cj = *cl.map_shared_rank(&cta_cnt, j);
             if (j < k) pre += cj;
             tot += cj;
             sum += *cl.map_shared_rank(&cta_sum, j);
+            bad |= *cl.map_shared_rank(&sh.bad, j);
         }
         cta_prefix = pre;
         if (k == 0) {
-            if (a.ncl) a.ncl[frame] = (int32_t)tot;
+            if (a.ncl) a.ncl[frame] = bad ? RS_FRAME_INVALID : (int32_t)tot;
             if (a.sizes) a.sizes[(size_t)frame * a.sizes_stride] = (int64_t)H * W - (int64_t)sum;
         }
     }

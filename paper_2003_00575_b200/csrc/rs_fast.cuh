@@ -53,6 +53,17 @@ namespace rs {
 #ifndef RS_STRIP_SETS
 #define RS_STRIP_SETS 4   // step A register sets: 4 = two-row prefetch, 3 = one-row prefetch
 #endif
+#ifdef RS_EXPERIMENTS   // phase ablation (scripts/ablation.py): leave after phase N, labels wrong
+#define RS_STOP(n)                \
+    if (a.stop_after == (n)) {    \
+        cl.sync();                \
+        return;                   \
+    }
+#else
+#define RS_STOP(n) \
+    do {           \
+    } while (0)
+#endif
 constexpr int kFastThreads = RS_FAST_THREADS;
 constexpr int kSweepUnroll = RS_SWEEP_UNROLL;
 constexpr int kFastOcc = RS_FAST_OCC;   // CTAs per SM the fast kernel is sized for
@@ -180,13 +191,18 @@ struct BitsStrip {
     int rfirst;   // first row walked (rstart, or a later row when rows are split between warps)
     int rowb;     // bytes per row (4 W)
     int wpb;      // bytes per plane row (4 WPR)
+    mutable uint32_t mx = 0;   // unsigned max of the raw bits loaded (input-contract screen)
 
     __device__ __forceinline__ void ld4(int r, float (&x)[4], bool pred = true) const {
         const float *p = col + (size_t)r * a.W;
 #pragma unroll
         for (int j = 0; j < 4; ++j)
-            if (pred && (FULL || cb + 32 * j < a.W)) x[j] = __ldg(p + 32 * j);
-            else if (!FULL) x[j] = 0.f;
+            if (pred && (FULL || cb + 32 * j < a.W)) {
+                x[j] = __ldg(p + 32 * j);
+                mx = max(mx, __float_as_uint(x[j]));
+            } else if (!FULL) {
+                x[j] = 0.f;
+            }
     }
 
     // va = row above, v = this row, vb = row below (read by ROW0 only); vn <-
@@ -365,6 +381,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
     extern __shared__ __align__(128) uint32_t sm[];
     __shared__ uint32_t warp_tot[kFastWarps];
     __shared__ uint32_t cta_cnt, cta_sum, ovf, ovf_any, n_edges, n_xedges, ucur;
+    __shared__ uint32_t cta_bad;       // a range of the band breaks the input contract (range_image.py:50-53)
     __shared__ uint32_t cta_pre[16];   // label base of every band of the cluster
     __shared__ uint32_t ovf_cnt[2];    // overflow path: kept roots and their cells in this band
     __shared__ uint32_t seam[2];   // seam edge per own row (R <= 64)
@@ -392,7 +409,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
     auto G = [&](int r, int c) -> float { return __ldg(fr + (size_t)r * W + c); };
 
     RS_MARK(0);
-    if (tid == 0) { seam[0] = seam[1] = 0; cta_sum = 0; n_edges = 0; n_xedges = 0; ucur = 0; }
+    if (tid == 0) { seam[0] = seam[1] = 0; cta_sum = 0; n_edges = 0; n_xedges = 0; ucur = 0; cta_bad = 0; }
 
     // ---- A. presence, left and up bits --------------------------------------
     // Row constants of the band (ground pair, height sine, vertical 2cos)
@@ -411,6 +428,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
     }
     __syncthreads();
     {
+        uint32_t umx = 0;   // input-contract screen over every range this thread loads
         // narrow frames: split each chunk's rows between S warps so that no
         // warp idles (a part starts one row early for its row-above values)
         const int nchunk = (W + 127) / 128;
@@ -425,9 +443,13 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
             const uint32_t sP = sb + 4u * a.o_P, sL = sb + 4u * a.o_L, sU = sb + 4u * a.o_U;
             const uint32_t sPh = sb + 4u * a.o_Ph, sLh = sb + 4u * a.o_Lh;
             const bool full = ch * 128 + 128 <= W && (WPR & 3) == 0;
-#define RS_STRIP(F, G)                                                                                     \
-    BitsStrip<F, MCA, G>{a, fr + cb, rowc, sP, sL, sU, sPh, sLh, MC, ch, lane, r0, rstart, rhi, cb, thr, tch, rlo, 4 * W, 4 * WPR} \
-        .run()
+#define RS_STRIP(F, G)                                                                                          \
+    do {                                                                                                    \
+        const BitsStrip<F, MCA, G> st{a, fr + cb, rowc, sP, sL, sU, sPh, sLh, MC, ch, lane, r0, rstart, rhi, cb, thr, \
+                                      tch, rlo, 4 * W, 4 * WPR};                                            \
+        st.run();                                                                                           \
+        umx = max(umx, st.mx);                                                                              \
+    } while (0)
             if (a.ground) {
                 if (full) RS_STRIP(true, true); else RS_STRIP(false, true);
             } else {
@@ -435,10 +457,19 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
             }
 #undef RS_STRIP
         }
+        if (__any_sync(kFull, umx > kMaxFiniteBits) && lane == 0) cta_bad = 1u;
     }
     __syncthreads();
+    if (cta_bad) {
+        // rare (a contract violation, or a -0.0): exact re-check of the band's own rows
+        bool b = false;
+        const float *own = fr + (size_t)r0 * W;
+        for (int i = tid; i < rows * W; i += kFastThreads) b |= !range_ok(__ldg(own + i));
+        b = __syncthreads_or(b);
+        if (tid == 0) cta_bad = b ? 1u : 0u;
+    }
     RS_MARK(1);
-    if (a.stop_after == 1) { cl.sync(); return; }
+    RS_STOP(1);
 
     // ---- B. edge words, seam, Map Connection bits ----------------------------
     // L = EH & P & (P shifted in from the left), U = EV & P & (P of the row
@@ -589,6 +620,20 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
     }
     __syncthreads();
     RS_MARK(2);
+    if (a.planes) {
+        // debug export (rs_fast_planes): P, L (bit 0 of a row = the seam edge),
+        // U and the Map Connection planes of the band's own rows, final here
+        const size_t fw = (size_t)H * WPR;
+        uint32_t *out = a.planes + (size_t)frame * (3 + a.n_off) * fw + (size_t)r0 * WPR;
+        for (int w = tid; w < nw; w += kFastThreads) {
+            const int q = divWPR(a, w);
+            const bool sm0 = (w - q * WPR) == 0 && ((seam[q >> 5] >> (q & 31)) & 1u);
+            out[w] = P[w];
+            out[fw + w] = L[w] | (sm0 ? 1u : 0u);
+            out[2 * fw + w] = U[w];
+            for (int o = 0; o < a.n_off; ++o) out[(3 + o) * fw + w] = MC[o * a.nwords + w];
+        }
+    }
 
     // ---- R. runs and their ids ------------------------------------------------
     // Warp `warp` owns words [wr0, wr1); a run continuing into the range gets a
@@ -635,7 +680,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
     }
     __syncthreads();
     RS_MARK(3);
-    if (a.stop_after == 2) { cl.sync(); return; }
+    RS_STOP(2);
 
     RunUF uf{E, cl, maskN, a.SHN, k};
     if (!overflow) {
@@ -723,7 +768,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
         gather(false);
         __syncthreads();
         RS_MARK(19);
-        if (a.stop_after == 9) { cl.sync(); return; }
+        RS_STOP(9);
         const uint32_t ne = n_edges;   // block-uniform
         if (ne > cap) {
             gather(true);
@@ -765,7 +810,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
         }
         __syncthreads();
         RS_MARK(4);
-    if (a.stop_after == 3) { cl.sync(); return; }
+    RS_STOP(3);
         // local flatten; LR marks the band-local roots
         for (uint32_t base = warp * 32; base < n_runs; base += kFastThreads) {
             const uint32_t id = base + lane;
@@ -824,7 +869,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
             carry = __shfl_sync(kFull, inc, 0);
         }
     }
-    if (a.stop_after == 4) { cl.sync(); return; }
+    RS_STOP(4);
     RS_MARK(6);
     cl.sync();   // #1: every band's runs are numbered, joined locally and sized
 
@@ -835,7 +880,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
     }
     __syncthreads();
     if (ovf_any) {   // cluster-uniform: union-find over cells in global memory (rs_overflow.cuh)
-        overflow_frame(a, P, L, U, Lh, MC, seam, ovf_cnt, warp_tot, frame);
+        overflow_frame(a, P, L, U, Lh, MC, seam, ovf_cnt, warp_tot, frame, &cta_bad);
         return;
     }
 
@@ -920,7 +965,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
         const uint32_t nx = min(n_xedges, xcap);
         for (uint32_t e = tid; e < nx; e += kFastThreads) uf.unite(XL[2 * e], XL[2 * e + 1]);
     }
-    if (a.stop_after == 5) { cl.sync(); return; }
+    RS_STOP(5);
     RS_MARK(8);
     cl.sync();   // #2: the forest is final
     RS_MARK(9);
@@ -936,7 +981,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
             atomicAdd(uf.slot(SZ, g), SZ[id]);
         }
     }
-    if (a.stop_after == 6) { cl.sync(); return; }
+    RS_STOP(6);
     RS_MARK(10);
     cl.sync();   // #3: sizes are final at every root
 
@@ -992,21 +1037,25 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
     cl.sync();   // #4: every band's kept bits, word prefixes and counts are published
     if (tid < a.C) {
         // label base of each band: kept roots of the bands before it
-        uint32_t pre = 0, tot = 0, sum = 0;
+        uint32_t pre = 0, tot = 0, sum = 0, bad = 0;
         for (int j = 0; j < a.C; ++j) {
             const uint32_t cj = *cl.map_shared_rank(&cta_cnt, j);
             if (j < tid) pre += cj;
             tot += cj;
-            if (tid == 0) sum += *cl.map_shared_rank(&cta_sum, j);
+            if (tid == 0) {
+                sum += *cl.map_shared_rank(&cta_sum, j);
+                bad |= *cl.map_shared_rank(&cta_bad, j);
+            }
         }
         cta_pre[tid] = pre;
         if (tid == 0 && k == 0) {
-            if (a.ncl) a.ncl[frame] = (int32_t)tot;
+            // RS_FRAME_INVALID marks a frame that breaks the input contract
+            if (a.ncl) a.ncl[frame] = bad ? RS_FRAME_INVALID : (int32_t)tot;
             if (a.sizes) a.sizes[(size_t)frame * a.sizes_stride] = (int64_t)H * W - (int64_t)sum;
         }
     }
     __syncthreads();
-    if (a.stop_after == 7) { cl.sync(); return; }
+    RS_STOP(7);
     RS_MARK(12);
 
     // ---- L. run labels straight from the root's band: label = band base +
@@ -1037,7 +1086,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
             SZ[id] = label;   // only this thread read SZ[id] (the root's size)
         }
     }
-    if (a.stop_after == 8) { cl.sync(); return; }
+    RS_STOP(8);
     RS_MARK(13);
     // #5, split: arrive now (this CTA reads no other CTA's shared memory after
     // this point), wait just before exiting (no CTA may exit while another

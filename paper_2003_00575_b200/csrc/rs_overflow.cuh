@@ -89,7 +89,7 @@ __device__ __forceinline__ void ovf_unite(int *par, int x, int y) {
 // every global access of a warp is one coalesced 128-byte row segment.
 __device__ RS_OVF_INLINE void overflow_frame(const KArgs &a, const uint32_t *P, const uint32_t *L, const uint32_t *U,
                                              const uint32_t *Lh, const uint32_t *MC, const uint32_t *seamw, uint32_t *cnt,
-                                             uint32_t *wtot, int frame) {
+                                             uint32_t *wtot, int frame, const uint32_t *bad) {
     cg::cluster_group cl = cg::this_cluster();
     const int k = (int)cl.block_rank();
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -200,16 +200,17 @@ __device__ RS_OVF_INLINE void overflow_frame(const KArgs &a, const uint32_t *P, 
     __syncthreads();
     if (lane == 0 && wsum) atomicAdd(cnt + 1, (uint32_t)wsum);
     cl.sync();
-    uint32_t base = 0, tot = 0;
+    uint32_t base = 0, tot = 0, anybad = 0;
     unsigned long long sum = 0;
     for (int j = 0; j < a.C; ++j) {
         const uint32_t cj = *cl.map_shared_rank(cnt, j);
         if (j < k) base += cj;
         tot += cj;
         sum += *cl.map_shared_rank(cnt + 1, j);
+        anybad |= *cl.map_shared_rank(bad, j);
     }
     if (k == 0 && tid == 0) {
-        if (a.ncl) a.ncl[frame] = (int32_t)tot;
+        if (a.ncl) a.ncl[frame] = anybad ? RS_FRAME_INVALID : (int32_t)tot;
         if (a.sizes) a.sizes[(size_t)frame * a.sizes_stride] = (int64_t)H * W - (int64_t)sum;
     }
     // roots: entry -> -(label + 1), label 0 = dropped

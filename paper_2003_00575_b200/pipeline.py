@@ -107,11 +107,22 @@ class BatchResult:
     """Device-side result of :meth:`Pipeline.segment_batch`."""
 
     labels: torch.Tensor          # int32 [B, H, W]
-    n_clusters: torch.Tensor      # int32 [B]
+    n_clusters: torch.Tensor      # int32 [B]; RS_FRAME_INVALID (-1) for a frame with bad ranges
     cluster_sizes: torch.Tensor | None   # int64 [B, stride]; row b valid up to n_clusters[b]
+
+    def check(self) -> "BatchResult":
+        """Raise the reference's ``ValueError`` (range_image.py:52-53) if a frame
+        held a NaN, inf or negative range (flagged by the kernel on the device;
+        this reads ``n_clusters`` back, so it synchronises)."""
+        bad = torch.nonzero(self.n_clusters == _native.RS_FRAME_INVALID).flatten()
+        if bad.numel():
+            raise ValueError(f"ranges must be finite and >= 0 (frame {int(bad[0])})")
+        return self
 
     def label_image(self, b: int) -> LabelImage:
         k = int(self.n_clusters[b])
+        if k == _native.RS_FRAME_INVALID:
+            raise ValueError(f"ranges must be finite and >= 0 (frame {b})")
         sizes = (self.cluster_sizes[b, :k + 1].cpu().numpy() if self.cluster_sizes is not None
                  else np.bincount(self.labels[b].cpu().numpy().ravel(), minlength=k + 1))
         return LabelImage(labels=self.labels[b].cpu().numpy(), cluster_sizes=sizes)
@@ -141,8 +152,8 @@ class Pipeline:
         if self.device.type == "cuda" and self.device.index is None and torch.cuda.is_available():
             self.device = torch.device("cuda", torch.cuda.current_device())
         self._tables = None
-        self._workspaces = {}
         self._tables_host = np.ascontiguousarray(self.packed.block, dtype=np.float32)
+        self._frame_bufs = None   # pinned staging of segment_range_image
 
     # -- helpers -----------------------------------------------------------
     @property
@@ -164,18 +175,6 @@ class Pipeline:
             self._tables = torch.from_numpy(self._tables_host).to(self.device)
         return self._tables
 
-    def _workspace(self, batch: int, stream):
-        """Device workspace the library asks for (none: rs_workspace_size is 0
-        for this library; kept so the ABI's workspace contract stays honoured)."""
-        need = int(_native.lib().rs_workspace_size(ctypes.byref(self.rs_config), batch))
-        if need <= 0:
-            return None
-        ws = self._workspaces.get(stream.cuda_stream)
-        if ws is None or ws.numel() < need:
-            ws = torch.zeros(need, dtype=torch.uint8, device=self.device)
-            self._workspaces[stream.cuda_stream] = ws
-        return ws
-
     def _check_frames(self, ranges: torch.Tensor):
         H, W = self.shape
         if ranges.dim() != 3 or tuple(ranges.shape[1:]) != (H, W):
@@ -184,37 +183,96 @@ class Pipeline:
         if ranges.dtype != torch.float32:
             raise ValueError(f"ranges must be float32, got {ranges.dtype}")
 
+    def _check_out(self, t: torch.Tensor, name: str, dtype, shape):
+        """Caller-supplied output buffers: dtype, shape, device, contiguity (the
+        C side writes through the raw pointer)."""
+        if not isinstance(t, torch.Tensor):
+            raise ValueError(f"{name} must be a torch.Tensor")
+        if t.dtype != dtype:
+            raise ValueError(f"{name} must be {dtype}, got {t.dtype}")
+        if t.device != self.device:
+            raise ValueError(f"{name} on {t.device}, pipeline on {self.device}")
+        if tuple(t.shape[:len(shape)]) != tuple(shape) or t.dim() != len(shape) + (name == "cluster_sizes"):
+            raise ValueError(f"{name} has shape {tuple(t.shape)}, expected {tuple(shape)}"
+                             + (" + (stride,)" if name == "cluster_sizes" else ""))
+        if not t.is_contiguous():
+            raise ValueError(f"{name} must be contiguous")
+
     # -- device batch ------------------------------------------------------
     def segment_batch(self, ranges: torch.Tensor, *, labels: torch.Tensor | None = None,
                       n_clusters: torch.Tensor | None = None,
                       cluster_sizes: torch.Tensor | bool | None = True,
                       stream: torch.cuda.Stream | None = None) -> BatchResult:
-        """Segment B frames resident on the GPU; asynchronous on ``stream``."""
+        """Segment B frames resident on the GPU; asynchronous on ``stream``.
+
+        The launch waits for the work already queued on the current stream
+        (the ranges' producer, the output allocations).  Frames with a NaN, inf
+        or negative range come back with ``n_clusters == -1``; ``.check()``
+        raises the reference's ``ValueError`` for them.
+        """
         self._require_cuda()
         self._check_frames(ranges)
         if ranges.device != self.device:
             raise ValueError(f"ranges on {ranges.device}, pipeline on {self.device}")
-        ranges = ranges.contiguous()
         B = ranges.shape[0]
         H, W = self.shape
-        if labels is None:
-            labels = torch.empty((B, H, W), dtype=torch.int32, device=self.device)
-        if n_clusters is None:
-            n_clusters = torch.empty((B,), dtype=torch.int32, device=self.device)
-        if cluster_sizes is True:
-            cluster_sizes = torch.empty((B, self.sizes_stride), dtype=torch.int64,
-                                        device=self.device)
-        elif cluster_sizes is False:
-            cluster_sizes = None
-        stride = cluster_sizes.shape[1] if cluster_sizes is not None else 0
-        s = stream if stream is not None else torch.cuda.current_stream(self.device)
-        ws = self._workspace(B, s)
-        st = _native.lib().rs_segment_batch(
-            ctypes.byref(self.rs_config), _ptr(self.device_tables()), _ptr(ranges), B,
-            _ptr(labels), _ptr(n_clusters), _ptr(cluster_sizes), stride,
-            _ptr(ws), 0 if ws is None else ws.numel(), ctypes.c_void_p(s.cuda_stream))
+        with torch.cuda.device(self.device):
+            cur = torch.cuda.current_stream(self.device)
+            ranges = ranges.contiguous()
+            if labels is None:
+                labels = torch.empty((B, H, W), dtype=torch.int32, device=self.device)
+            else:
+                self._check_out(labels, "labels", torch.int32, (B, H, W))
+            if n_clusters is None:
+                n_clusters = torch.empty((B,), dtype=torch.int32, device=self.device)
+            else:
+                self._check_out(n_clusters, "n_clusters", torch.int32, (B,))
+            if cluster_sizes is True:
+                cluster_sizes = torch.empty((B, self.sizes_stride), dtype=torch.int64,
+                                            device=self.device)
+            elif cluster_sizes is False or cluster_sizes is None:
+                cluster_sizes = None
+            else:
+                self._check_out(cluster_sizes, "cluster_sizes", torch.int64, (B,))
+                if cluster_sizes.shape[1] < self.sizes_stride:
+                    raise ValueError(f"cluster_sizes needs >= {self.sizes_stride} columns, "
+                                     f"got {cluster_sizes.shape[1]}")
+            stride = cluster_sizes.shape[1] if cluster_sizes is not None else 0
+            s = stream if stream is not None else cur
+            if s.cuda_stream != cur.cuda_stream:
+                s.wait_stream(cur)
+                for t in (ranges, labels, n_clusters, cluster_sizes, self.device_tables()):
+                    if t is not None:
+                        t.record_stream(s)
+            st = _native.lib().rs_segment_batch(
+                ctypes.byref(self.rs_config), _ptr(self.device_tables()), _ptr(ranges), B,
+                _ptr(labels), _ptr(n_clusters), _ptr(cluster_sizes), stride,
+                ctypes.c_void_p(s.cuda_stream))
         _native.check(st, "rs_segment_batch")
         return BatchResult(labels, n_clusters, cluster_sizes)
+
+    def fast_planes(self, ranges: torch.Tensor):
+        """The fused kernel's own edge decisions (``rs_fast_planes``): returns
+        ``(planes uint32 [B, 3 + n_offsets, H, ceil(W/32)], BatchResult)``;
+        planes: presence, left edge, up edge, then one per Map Connection offset
+        (include/rangeseg_b200.h).  For parity checks."""
+        self._require_cuda()
+        self._check_frames(ranges)
+        B = ranges.shape[0]
+        H, W = self.shape
+        wpr = (W + 31) // 32
+        with torch.cuda.device(self.device):
+            ranges = ranges.contiguous()
+            planes = torch.zeros((B, 3 + len(self.packed.offsets), H, wpr), dtype=torch.int32,
+                                 device=self.device)
+            labels = torch.empty((B, H, W), dtype=torch.int32, device=self.device)
+            ncl = torch.empty((B,), dtype=torch.int32, device=self.device)
+            st = _native.lib().rs_fast_planes(
+                ctypes.byref(self.rs_config), _ptr(self.device_tables()), _ptr(ranges), B,
+                _ptr(planes), _ptr(labels), _ptr(ncl),
+                ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream))
+        _native.check(st, "rs_fast_planes")
+        return planes, BatchResult(labels, ncl, None)
 
     def stage_masks(self, ranges: torch.Tensor):
         """(ground, horizontal, vertical) bool CUDA tensors — extract_ground and
@@ -251,14 +309,32 @@ class Pipeline:
         if not ranges.flags.c_contiguous:
             raise ValueError("ranges must be C-contiguous")
         B = ranges.shape[0]
+
+        def out(a, name, dtype, shape):
+            if not isinstance(a, np.ndarray) or a.dtype != dtype or a.shape[:len(shape)] != shape \
+                    or not a.flags.c_contiguous or not a.flags.writeable:
+                raise ValueError(f"{name} must be a writeable C-contiguous {np.dtype(dtype).name} "
+                                 f"array of shape {shape}" + (" + (stride,)" if name == "cluster_sizes" else ""))
+            if a.ndim != len(shape) + (name == "cluster_sizes"):
+                raise ValueError(f"{name} has {a.ndim} dimensions")
+
         if labels is None:
             labels = np.empty((B, H, W), dtype=np.int32)
+        else:
+            out(labels, "labels", np.int32, (B, H, W))
         if n_clusters is None:
             n_clusters = np.empty((B,), dtype=np.int32)
+        else:
+            out(n_clusters, "n_clusters", np.int32, (B,))
         if cluster_sizes is True:
             cluster_sizes = np.empty((B, self.sizes_stride), dtype=np.int64)
-        elif cluster_sizes is False:
+        elif cluster_sizes is False or cluster_sizes is None:
             cluster_sizes = None
+        else:
+            out(cluster_sizes, "cluster_sizes", np.int64, (B,))
+            if cluster_sizes.shape[1] < self.sizes_stride:
+                raise ValueError(f"cluster_sizes needs >= {self.sizes_stride} columns, "
+                                 f"got {cluster_sizes.shape[1]}")
         stride = cluster_sizes.shape[1] if cluster_sizes is not None else 0
         with torch.cuda.device(self.device):
             st = _native.lib().rs_segment_batch_host(
@@ -271,24 +347,70 @@ class Pipeline:
         return labels, n_clusters, cluster_sizes
 
     # -- the reference's per-frame entry point --------------------------------
+    def _frame_buffers(self):
+        """Pinned host staging + device buffers of segment_range_image, made once."""
+        if self._frame_bufs is None:
+            H, W = self.shape
+            pin = dict(pin_memory=True)
+            self._frame_bufs = {
+                "h_in": torch.empty((1, H, W), dtype=torch.float32, **pin),
+                "h_lab": torch.empty((1, H, W), dtype=torch.int32, **pin),
+                "h_ncl": torch.empty((1,), dtype=torch.int32, **pin),
+                "h_sz": torch.empty((1, self.sizes_stride), dtype=torch.int64, **pin),
+                "d_in": torch.empty((1, H, W), dtype=torch.float32, device=self.device),
+                "d_lab": torch.empty((1, H, W), dtype=torch.int32, device=self.device),
+                "d_ncl": torch.empty((1,), dtype=torch.int32, device=self.device),
+                "d_sz": torch.empty((1, self.sizes_stride), dtype=torch.int64, device=self.device),
+                "ev": [torch.cuda.Event(enable_timing=True) for _ in range(3)],
+            }
+        return self._frame_bufs
+
     def segment_range_image(self, ri: RangeImage):
-        """Cluster one image-shaped frame; returns ``(LabelImage, TimingRecord)``."""
+        """Cluster one image-shaped frame (pipeline.py:85-131); returns
+        ``(LabelImage, TimingRecord)``.
+
+        One frame through pinned staging: H2D copy, the fused kernel, D2H of
+        labels / count / sizes, one synchronisation.  A raw array gets
+        ``from_ranges``' contract (finite, >= 0: ``ValueError``), checked by
+        the kernel as it reads the ranges; a ``RangeImage`` is taken as is, like
+        the reference (a NaN or negative range is then simply no return).
+        ``TimingRecord.ccl`` = device time of the fused kernel (every stage of
+        the reference runs inside it), ``total`` = wall time of the call.
+        """
         rec = TimingRecord()
         t0 = time.perf_counter()
-        ranges = ri.ranges if isinstance(ri, RangeImage) else from_ranges(ri).ranges
+        ranges = ri.ranges if isinstance(ri, RangeImage) else np.asarray(ri)
+        if ranges.ndim != 2:
+            raise ValueError(f"range image must be 2-D, got shape {ranges.shape}")
         if ranges.shape != self.shape:
             raise ValueError(f"range image {ranges.shape} does not match model {self.shape}")
         self._require_cuda()
-        x = torch.from_numpy(np.ascontiguousarray(ranges, dtype=np.float32)).to(
-            self.device, non_blocking=False)[None]
-        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        ev0.record()
-        res = self.segment_batch(x)
-        ev1.record()
-        k = int(res.n_clusters[0].item())
-        li = LabelImage(labels=res.labels[0].cpu().numpy(),
-                        cluster_sizes=res.cluster_sizes[0, :k + 1].cpu().numpy())
-        rec.ccl = ev0.elapsed_time(ev1)
+        b = self._frame_buffers()
+        np.copyto(b["h_in"].numpy()[0], ranges, casting="same_kind")
+        with torch.cuda.device(self.device):
+            s = torch.cuda.current_stream(self.device)
+            ev = b["ev"]
+            b["d_in"].copy_(b["h_in"], non_blocking=True)
+            ev[0].record(s)
+            st = _native.lib().rs_segment_batch(
+                ctypes.byref(self.rs_config), _ptr(self.device_tables()), _ptr(b["d_in"]), 1,
+                _ptr(b["d_lab"]), _ptr(b["d_ncl"]), _ptr(b["d_sz"]), self.sizes_stride,
+                ctypes.c_void_p(s.cuda_stream))
+            _native.check(st, "rs_segment_batch")
+            ev[1].record(s)
+            b["h_lab"].copy_(b["d_lab"], non_blocking=True)
+            b["h_ncl"].copy_(b["d_ncl"], non_blocking=True)
+            b["h_sz"].copy_(b["d_sz"], non_blocking=True)
+            ev[2].record(s)
+            ev[2].synchronize()
+        k = int(b["h_ncl"][0])
+        labels = b["h_lab"].numpy()[0].copy()
+        if k == _native.RS_FRAME_INVALID:
+            if not isinstance(ri, RangeImage):
+                raise ValueError("ranges must be finite and >= 0")
+            k = int(labels.max())   # labels are 1..K, each kept cluster has cells
+        li = LabelImage(labels=labels, cluster_sizes=b["h_sz"].numpy()[0, :k + 1].copy())
+        rec.ccl = ev[0].elapsed_time(ev[1])
         rec.total = (time.perf_counter() - t0) * 1e3
         return li, rec
 
@@ -364,5 +486,7 @@ def segment_in_parallel(range_images, model: SensorModel,
     labels = res.labels.cpu().numpy()
     ncl = res.n_clusters.cpu().numpy()
     sizes = res.cluster_sizes.cpu().numpy()
+    for b in np.nonzero(ncl == _native.RS_FRAME_INVALID)[0]:   # RangeImage inputs are taken as is
+        ncl[b] = labels[b].max()
     return [LabelImage(labels=labels[b], cluster_sizes=sizes[b, :int(ncl[b]) + 1].copy())
             for b in range(len(frames))]

@@ -132,3 +132,25 @@ def eval_case(key):
     matches = [tuple(m) for m in json.loads(str(st[f"{key}/matches"][0]))]
     summary = json.loads(str(st[f"{key}/summary"][0]))
     return st[f"{key}/gt"], st[f"{key}/pred"], int(st[f"{key}/min_gt_points"]), matches, summary
+
+
+def pack_bits(bits):
+    """bool [..., W] -> uint32 [..., ceil(W/32)], bit c%32 of word c/32 (the
+    rs_fast_planes layout)."""
+    bits = np.asarray(bits, dtype=bool)
+    W = bits.shape[-1]
+    wpr = (W + 31) // 32
+    pad = np.zeros(bits.shape[:-1] + (wpr * 32,), dtype=bool)
+    pad[..., :W] = bits
+    return np.packbits(pad, axis=-1, bitorder="little").view(np.uint32)
+
+
+def planes_from_masks(ranges, ground, horizontal, vertical):
+    """Presence / left-edge / up-edge planes from the reference's stage outputs
+    (extract_ground mask, build_connectivity horizontal / vertical images)."""
+    H, W = ranges.shape
+    pres = (ranges > 0) & ~ground
+    left = np.roll(horizontal, 1, axis=1) if W > 1 else np.zeros_like(horizontal)
+    up = np.zeros((H, W), dtype=bool)
+    up[1:] = vertical
+    return np.stack([pack_bits(pres), pack_bits(left), pack_bits(up)])

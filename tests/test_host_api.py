@@ -131,7 +131,7 @@ def test_library_exports_every_header_symbol():
     assert declared == set(_native.EXPORTS)
     for name in declared:
         assert hasattr(lib, name), name
-    assert lib.rs_version() == 201
+    assert lib.rs_version() == 300
 
 
 def test_tables_count_matches_layout():
@@ -178,3 +178,73 @@ def test_pipeline_refuses_cpu_device():
     import torch
     with pytest.raises(RuntimeError, match="no CPU fallback"):
         pipe.segment_batch(torch.zeros((1, 8, 16)))
+
+
+def test_reserved_fields_rejected():
+    """reserved[1]/[2] are experiment hooks: a production build rejects them."""
+    m = rs.fov_model(8, 2.0, -20.0, 16, 1.7)
+    cfg = _native.make_config(rs.pack_tables(m, rs.PipelineConfig()))
+    cfg.reserved[1] = 3
+    with pytest.raises(ValueError, match="reserved"):
+        _native.plan(cfg)
+    cfg.reserved[1] = 0
+    cfg.reserved[2] = 1
+    with pytest.raises(ValueError, match="reserved"):
+        _native.plan(cfg)
+
+
+def test_plan_prefers_fast_kernel_when_dense_cannot_hold():
+    """H=512, W=1024: no dense plan (17 bands of 31 rows) but 8 fast bands fit."""
+    m = rs.fov_model(512, 20.0, -20.0, 1024, 1.7)
+    cfg = _native.make_config(rs.pack_tables(m, rs.PipelineConfig(ground_removal=False)))
+    d = _native.plan_detail(cfg)
+    assert d["fast"] == 1 and d["fast_ctas"] <= 16
+
+
+def _host_call(cfg, batch, sizes_stride, with_sizes=True):
+    import ctypes
+    lib = _native.lib()
+    H, W = cfg.height, cfg.width
+    tab = np.zeros(lib.rs_tables_count(H, cfg.n_offsets), np.float32)
+    rg = np.zeros((max(batch, 1), H, W), np.float32)
+    lab = np.zeros((max(batch, 1), H, W), np.int32)
+    ncl = np.zeros(max(batch, 1), np.int32)
+    sz = np.zeros((max(batch, 1), max(sizes_stride, 1)), np.int64)
+    p = lambda a: a.ctypes.data_as(ctypes.c_void_p)   # noqa: E731
+    return lib.rs_segment_batch_host(ctypes.byref(cfg), p(tab), p(rg), batch, p(lab), p(ncl),
+                                     p(sz) if with_sizes else None, sizes_stride)
+
+
+def test_host_entry_checks_sizes_stride_before_any_launch():
+    m = rs.fov_model(8, 2.0, -20.0, 16, 1.7)
+    cfg = _native.make_config(rs.pack_tables(m, rs.PipelineConfig(min_cluster_points=1)))
+    need = 8 * 16 + 1
+    assert _host_call(cfg, 2, need - 1) == _native.RS_EINVAL
+    assert b"sizes_stride" in _native.lib().rs_last_error()
+    assert _host_call(cfg, 2, -5) == _native.RS_EINVAL
+    assert _host_call(cfg, -1, need) == _native.RS_EINVAL
+    assert _host_call(cfg, 0, need) == _native.RS_OK
+
+
+def test_device_entry_checks_alignment_and_stride():
+    import ctypes
+    lib = _native.lib()
+    m = rs.fov_model(8, 2.0, -20.0, 128, 1.7)
+    cfg = _native.make_config(rs.pack_tables(m, rs.PipelineConfig(min_cluster_points=1)))
+    fake = ctypes.c_void_p(0x10000)
+    # misaligned labels pointer
+    st = lib.rs_segment_batch(ctypes.byref(cfg), fake, fake, 1, ctypes.c_void_p(0x10004), fake, None, 0, None)
+    assert st == _native.RS_EINVAL and b"aligned" in lib.rs_last_error()
+    st = lib.rs_segment_batch(ctypes.byref(cfg), fake, fake, 1, fake, fake, fake, 10, None)
+    assert st == _native.RS_EINVAL and b"sizes_stride" in lib.rs_last_error()
+
+
+def test_plan_cache_keeps_errors_per_config():
+    m = rs.fov_model(8, 2.0, -20.0, 16, 1.7)
+    good = _native.make_config(rs.pack_tables(m, rs.PipelineConfig()))
+    bad = _native.make_config(rs.pack_tables(m, rs.PipelineConfig()))
+    bad.rows_per_cta = 99
+    for _ in range(3):
+        assert _native.plan(good)[1] >= 1
+        with pytest.raises(ValueError, match="rows_per_cta"):
+            _native.plan(bad)

@@ -71,3 +71,38 @@ def test_oracle_labels_to_points_matches_reference(key):
     m, c = golden.project_case(key)
     got = oracle.labels_to_points(c["labels"], c["point_index"], c["counts"][0])
     assert np.array_equal(got, c["point_labels"])
+
+
+@pytest.mark.parametrize("case_key,frame_key", golden.frame_cases())
+def test_oracle_planes_match_reference_stage_masks(case_key, frame_key):
+    """oracle.planes_batch (the layout the GPU parity export is checked in)
+    against the reference's recorded extract_ground / build_connectivity."""
+    m, cfg, ranges, labels, sizes, stages = golden.case("frames", case_key, frame_key)
+    if stages is None:
+        pytest.skip("no stage masks recorded for this case")
+    pl = oracle.planes_batch(ranges[None], pack_tables(m, cfg), nthreads=1)[0]
+    assert np.array_equal(pl[:3], golden.planes_from_masks(ranges, *stages))
+
+
+def test_oracle_mc_planes_equal_literal_rule():
+    """Map Connection planes: the decision of map_connections.py:155-169 for
+    every present pair, restated here in numpy on a small random frame."""
+    import paper_2003_00575_b200 as rs
+    g = np.random.default_rng(5)
+    m = rs.fov_model(20, 2.0, -20.0, 70, 1.7)
+    cfg = rs.PipelineConfig(mc_pattern=rs.preset_pattern("mc14"), min_cluster_points=1)
+    pt = pack_tables(m, cfg)
+    fr = (g.uniform(3, 6, (20, 70)) * (g.random((20, 70)) > 0.2)).astype(np.float32)
+    pl = oracle.planes_batch(fr[None], pt, nthreads=1)[0]
+    pres = np.unpackbits(pl[0].view(np.uint8), bitorder="little").reshape(20, -1)[:, :70].astype(bool)
+    H, W = fr.shape
+    for k, (dy, dx) in enumerate(pt.offsets):
+        want = np.zeros((H, W), bool)
+        tc = pt.block[H + 5 * (H - 1) + k * H: H + 5 * (H - 1) + (k + 1) * H]
+        for r in range(dy, H):
+            for c in range(W):
+                ur, uc = r - dy, (c - dx) % W
+                a, b = np.float32(fr[ur, uc]), np.float32(fr[r, c])
+                d = (a * a + b * b) - np.float32(tc[ur]) * (a * b)
+                want[r, c] = pres[r, c] and pres[ur, uc] and d <= np.float32(pt.d_max_sq)
+        assert np.array_equal(pl[3 + k], golden.pack_bits(want)), (dy, dx)
