@@ -55,6 +55,8 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=10.0)
     p.add_argument("--no-cloud", action="store_true", help="skip the point-cloud path measurement")
+    p.add_argument("--no-per-config", action="store_true", help="skip the per-config block")
+    p.add_argument("--no-check", action="store_true", help="skip the parity checks against the oracle")
     return p.parse_args()
 
 
@@ -253,12 +255,69 @@ def cloud_bench(args, pipe, frames, spec, flush):
     return out
 
 
+def ref_pipe_args(args, spec):
+    """Arguments of baseline/ref_bench.make_pipeline for this workload."""
+    import paper_2003_00575_b200 as rs
+    cfg = pipeline_config(args)
+    return dict(H=spec.H, W=spec.W, top_deg=spec.top_deg, bottom_deg=spec.bottom_deg, mount=spec.mount,
+                offsets=tuple(cfg.mc_pattern.offsets), ground=cfg.ground_removal,
+                min_points=cfg.min_cluster_points)
+
+
 def run_reference(args):
-    """CPU arm: the reference algorithm (C oracle port) on all host threads."""
+    """CPU arm: the UNMODIFIED reference (baseline/_ref, pure Python + numba)
+    through its public Pipeline API, one process per host core; falls back to
+    the C port of the reference algorithm (oracle/) if it is not installed."""
     rank, _, world = dist_env()
     if rank != 0:
         return
-    import numpy as np  # noqa: F401
+    from baseline import ref_bench
+    from paper_2003_00575_b200 import synthetic
+    spec = synthetic.CONFIGS[args.config]
+    rangeseg, why = ref_bench.load()
+    if rangeseg is None:
+        return run_reference_port(args, why)
+    # a bounded sample of the workload: its first frames (seeds 0..n-1),
+    # generated on the host (no CUDA in this process: the workers fork)
+    n = min(spec.batch, 32)
+    frames = synthetic.make_batch(args.config, n, device="cpu").numpy()
+    pa = ref_pipe_args(args, spec)
+    one = ref_bench.single_core(frames[:16], pa, min_seconds=3.0)
+    nproc = os.cpu_count() or 1
+    per_proc = max(1, int(round(0.25 * one["frames_per_s"])))   # ~0.25 s of work per process and step
+    pool = ref_bench.AllCores(frames, pa, nproc)
+    for _ in range(args.warmup):
+        pool.step(per_proc)
+    done, tot = 0, 0.0
+    for _ in range(args.steps):
+        d, el = pool.step(per_proc)
+        done += d
+        tot += el
+    pool.close()
+    fps = done / tot
+    cells = spec.H * spec.W
+    line = {
+        "impl": "reference", "metric": "frames/s", "value": fps, "unit": "frames/s",
+        "points_per_s": fps * cells, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": tot / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded BASELINE generator)",
+        "config": workload_config(args, spec, spec.batch, 1),
+        "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": nproc, "kind": "reference",
+                         "sample": f"{per_proc} frames per process and step cycling over the workload's first "
+                                   f"{n} frames; {nproc} processes (one per core, pinned), each with its own "
+                                   "rangeseg.Pipeline from baseline/_ref (unmodified reference, "
+                                   "segment_range_image)",
+                         "cpu_model": ref_bench.cpu_model()},
+        "single_core": dict(one, semantics="rangeseg.bench_run: 1 pinned core, GC off, warm-up 3, "
+                                           "per-frame TimingRecord.total"),
+        "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_reference_port(args, why):
+    """Fallback reference arm: the C port of the reference algorithm (oracle/)."""
+    rank, _, world = dist_env()
     import torch
     import paper_2003_00575_b200 as rs
     from oracle import oracle
@@ -293,10 +352,135 @@ def run_reference(args):
         "config": workload_config(args, spec, B, 1),
         "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": nthreads, "kind": "port",
                          "sample": f"{sample} of the {B} frames per step, oracle/rangeseg_oracle.c "
-                                   f"(reference algorithm restated in C), {nthreads} threads"},
+                                   f"(reference algorithm restated in C), {nthreads} threads",
+                         "why_not_reference": why},
         "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+PER_CONFIG = (   # (label, config id, skip S, core, preset)
+    ("c0", 0, 0, False, None), ("c1", 1, 0, False, None), ("c2", 2, 0, False, None),
+    ("c3", 3, 0, False, None), ("c4", 4, 0, False, None), ("c1_core", 1, 0, True, None),
+    ("c4_core", 4, 0, True, None), ("c1_S1", 1, 1, False, None), ("c1_mc6", 1, 0, False, "mc6"),
+    ("c1_mc14", 1, 0, False, "mc14"),
+)
+
+
+def variant_config(core, skip, preset):
+    import paper_2003_00575_b200 as rs
+    pat = rs.preset_pattern(preset) if preset else rs.skip_pattern(skip)
+    if core:
+        return rs.PipelineConfig(mc_pattern=pat, ground_removal=False, min_cluster_points=1)
+    return rs.PipelineConfig(mc_pattern=pat)
+
+
+def parity_check(pipe, frames):
+    """The fused kernel against the CPU oracle on the same frames: frames whose
+    labels / count / sizes differ, and the kernel's OWN edge decisions
+    (rs_fast_planes: presence, left, up and Map Connection bits) against the
+    oracle's, as a count of differing decisions (north_star's mismatch count)."""
+    import numpy as np
+    import torch
+    from oracle import oracle
+    res = pipe.segment_batch(frames)
+    host = frames.cpu().numpy()
+    wl, wn, ws = oracle.segment_batch(host, pipe.packed, sizes_stride=pipe.sizes_stride)
+    torch.cuda.synchronize()
+    gl, gn, gs = res.labels.cpu().numpy(), res.n_clusters.cpu().numpy(), res.cluster_sizes.cpu().numpy()
+    bad = 0
+    for b in range(host.shape[0]):
+        k = int(wn[b])
+        if gn[b] != wn[b] or not np.array_equal(gl[b], wl[b]) or not np.array_equal(gs[b, :k + 1], ws[b, :k + 1]):
+            bad += 1
+    out = {"frames_checked": int(host.shape[0]), "label_mismatch_frames": bad}
+    if pipe.plan["fast"]:
+        planes, _ = pipe.fast_planes(frames)
+        want = oracle.planes_batch(host, pipe.packed)
+        got = planes.cpu().numpy().view(np.uint32)
+        out["edge_decisions_checked"] = int(want.size * 32)
+        out["edge_mismatches"] = int(np.unpackbits((got ^ want).view(np.uint8)).sum())
+    return out
+
+
+def time_kernel(pipe, frames, labels, ncl, sizes, steps, flush, stream):
+    import torch
+    for _ in range(3):
+        pipe.segment_batch(frames, labels=labels, n_clusters=ncl, cluster_sizes=sizes)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    torch.cuda.synchronize()
+    for a, b in ev:
+        flush.zero_()
+        a.record(stream)
+        pipe.segment_batch(frames, labels=labels, n_clusters=ncl, cluster_sizes=sizes)
+        b.record(stream)
+    torch.cuda.synchronize()
+    return sum(a.elapsed_time(b) for a, b in ev) / steps
+
+
+def per_config_block(args, dev, flush, peak):
+    """Every BASELINE config (reference defaults) plus the core / skip /
+    Map Connection variants: kernel ms per batch, frames/s, roofline fraction
+    (16.5 B/cell + 0.25 per offset) and compulsory fraction (8 B/cell), and
+    the parity check of each against the oracle at its full batch."""
+    import torch
+    import paper_2003_00575_b200 as rs
+    from paper_2003_00575_b200 import synthetic
+    out = {}
+    stream = torch.cuda.current_stream(dev)
+    cache = {}
+    for label, cid, skip, core, preset in PER_CONFIG:
+        spec = synthetic.CONFIGS[cid]
+        if cid not in cache:
+            cache.clear()
+            cache[cid] = synthetic.make_batch(cid, device=dev)
+        frames = cache[cid]
+        B = frames.shape[0]
+        cfg = variant_config(core, skip, preset)
+        pipe = rs.Pipeline(synthetic.sensor_for(spec), cfg, device=dev)
+        labels = torch.empty((B, spec.H, spec.W), dtype=torch.int32, device=dev)
+        ncl = torch.empty((B,), dtype=torch.int32, device=dev)
+        sizes = torch.empty((B, pipe.sizes_stride), dtype=torch.int64, device=dev)
+        ms = time_kernel(pipe, frames, labels, ncl, sizes, 30, flush, stream)
+        cells = B * spec.H * spec.W
+        bpc = ALGO_BYTES_PER_CELL + MC_BYTES_PER_OFFSET * len(cfg.mc_pattern)
+        e = {"frames": B, "H": spec.H, "W": spec.W, "offsets": len(cfg.mc_pattern),
+             "params": ("core" if core else "defaults") + (f", {preset}" if preset else f", S={skip}"),
+             "ms": ms, "frames_per_s": B / (ms * 1e-3), "points_per_s": cells / (ms * 1e-3),
+             "bytes_per_cell": bpc, "frac": cells * bpc / (ms * 1e-3) / 1e9 / peak,
+             "compulsory_frac": cells * COMPULSORY_BYTES_PER_CELL / (ms * 1e-3) / 1e9 / peak,
+             "plan": {"rows_per_cta": pipe.rows_per_cta, "ctas_per_frame": pipe.ctas_per_frame,
+                      "fast": bool(pipe.plan["fast"])}}
+        if not args.no_check:
+            e.update(parity_check(pipe, frames))
+        out[label] = e
+    return out
+
+
+def per_frame_api(args, dev, n=300):
+    """The reference's own per-frame entry (pipeline.py:85-131) through this
+    package: Pipeline.segment_range_image on single 64x2048 frames, numpy in
+    and numpy out (H2D, kernel, D2H, one sync), wall-clock latency per call."""
+    import numpy as np
+    import paper_2003_00575_b200 as rs
+    from paper_2003_00575_b200 import synthetic
+    spec = synthetic.CONFIGS[0]
+    frames = synthetic.make_batch(1, 8, device=dev).cpu().numpy()
+    pipe = rs.Pipeline(synthetic.sensor_for(spec), rs.PipelineConfig(), device=dev)
+    for i in range(10):
+        pipe.segment_range_image(frames[i % 8])
+    t, k = [], []
+    for i in range(n):
+        t0 = time.perf_counter()
+        _, rec = pipe.segment_range_image(frames[i % 8])
+        t.append((time.perf_counter() - t0) * 1e3)
+        k.append(rec.ccl)
+    t = np.array(t)
+    return {"calls": n, "ms_p50": float(np.percentile(t, 50)), "ms_p99": float(np.percentile(t, 99)),
+            "ms_mean": float(t.mean()), "kernel_ms_p50": float(np.percentile(k, 50)),
+            "frames_per_s": 1e3 / float(t.mean()),
+            "path": "Pipeline.segment_range_image(numpy [64, 2048] float32) -> LabelImage; pinned staging, "
+                    "rs_segment_batch, one sync; config-0 geometry, reference defaults"}
 
 
 def run_b200(args):
@@ -396,12 +580,32 @@ def run_b200(args):
     if not args.no_cloud and world == 1:
         cloud_path = cloud_bench(args, pipe, frames, spec, flush)
 
-    cpu = None
+    cpu = cpu_port = None
     if not args.no_cpu_baseline:
         done, el = cpu_sample(frames.cpu().numpy(), pipe.packed, args.cpu_seconds, 1)
-        cpu = {"value": done / el, "unit": "frames/s", "cores": 1, "kind": "port",
-               "sample": f"{done} frames of this workload, single thread, oracle/rangeseg_oracle.c "
-                         f"(reference algorithm restated in C), {el:.1f} s"}
+        cpu_port = {"value": done / el, "unit": "frames/s", "cores": 1, "kind": "port",
+                    "sample": f"{done} frames of this workload, single thread, oracle/rangeseg_oracle.c "
+                              f"(reference algorithm restated in C), {el:.1f} s"}
+        from baseline import ref_bench
+        if ref_bench.load()[0] is not None:
+            one = ref_bench.single_core(frames[:16].cpu().numpy(), ref_pipe_args(args, spec),
+                                        min_seconds=args.cpu_seconds)
+            cpu = {"value": one["frames_per_s"], "unit": "frames/s", "cores": 1, "kind": "reference",
+                   "sample": f"the workload's first 16 frames, {one['frames_timed']} frame timings; "
+                             "rangeseg.bench_run (unmodified reference from baseline/_ref: 1 pinned core, "
+                             "GC off, warm-up 3, per-frame TimingRecord.total)",
+                   "ms_p50": one["ms_p50"], "ms_p99": one["ms_p99"], "cpu_model": ref_bench.cpu_model(),
+                   "host_cores": os.cpu_count()}
+        else:
+            cpu = cpu_port
+
+    per_config = None
+    if not args.no_per_config and world == 1:
+        per_config = per_config_block(args, dev, flush, peak)
+    frame_api = per_frame_api(args, dev) if world == 1 else None
+    check = None
+    if not args.no_check:
+        check = parity_check(pipe, frames)
 
     traffic = None
     tf = ROOT / "profiles" / "kernel_traffic.json"
@@ -428,7 +632,13 @@ def run_b200(args):
                      "peak_source": peak_src, "kernel": "rs_fast_kernel (one launch per step; node-capacity overflow handled in-kernel)",
                      "kernel_ms": ms},
         "cpu_baseline": cpu,
+        "cpu_baseline_port": cpu_port,
         "e2e": e2e,
+        "edge_mismatches": None if check is None else check.get("edge_mismatches"),
+        "frames_checked": None if check is None else check["frames_checked"],
+        "parity": check,
+        "per_frame_api": frame_api,
+        "per_config": per_config,
         "cloud_path": cloud_path,
         "gpu_launches": args.steps,   # one rs_fast_kernel (or rs_dense_kernel) launch per step
         "clocks": clk.summary(),

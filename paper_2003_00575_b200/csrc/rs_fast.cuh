@@ -191,7 +191,7 @@ struct BitsStrip {
     int rfirst;   // first row walked (rstart, or a later row when rows are split between warps)
     int rowb;     // bytes per row (4 W)
     int wpb;      // bytes per plane row (4 WPR)
-    mutable uint32_t mx = 0;   // unsigned max of the raw bits loaded (input-contract screen)
+    mutable uint32_t mx = 0;   // unsigned max of the raw bits of the rows walked (input-contract screen)
 
     __device__ __forceinline__ void ld4(int r, float (&x)[4], bool pred = true) const {
         const float *p = col + (size_t)r * a.W;
@@ -199,7 +199,6 @@ struct BitsStrip {
         for (int j = 0; j < 4; ++j)
             if (pred && (FULL || cb + 32 * j < a.W)) {
                 x[j] = __ldg(p + 32 * j);
-                mx = max(mx, __float_as_uint(x[j]));
             } else if (!FULL) {
                 x[j] = 0.f;
             }
@@ -227,6 +226,11 @@ struct BitsStrip {
         uint32_t pw[4], lw[4], uw[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
+#ifndef RS_NO_SCREEN
+            // input-contract screen on the row being decided (every row of the
+            // walk is the current row exactly once; no wait on a prefetch)
+            mx = max(mx, __float_as_uint(v[j]));
+#endif
             const float d1 = ROW0 ? v[j] : va[j];
             const float d2 = ROW0 ? vb[j] : v[j];
             const bool gr = GROUND && ground_fast(c.x, c.y, c.z, c.w, c2.x, c2.z, d1, d2, v[j], ROW0 ? vb[j] : va[j]);
@@ -620,6 +624,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
     }
     __syncthreads();
     RS_MARK(2);
+#ifndef RS_NO_PLANES
     if (a.planes) {
         // debug export (rs_fast_planes): P, L (bit 0 of a row = the seam edge),
         // U and the Map Connection planes of the band's own rows, final here
@@ -634,6 +639,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
             for (int o = 0; o < a.n_off; ++o) out[(3 + o) * fw + w] = MC[o * a.nwords + w];
         }
     }
+#endif
 
     // ---- R. runs and their ids ------------------------------------------------
     // Warp `warp` owns words [wr0, wr1); a run continuing into the range gets a
