@@ -130,7 +130,10 @@ size_t dense_layout(int R, int W, int n_off, KArgs *k) {
 }
 
 // ---- fast kernel layout ---------------------------------------------------------
-size_t fast_layout(int R, int W, int n_off, int NC, KArgs *k) {
+// No Map Connection planes: the offsets are tested after the band-local
+// union-find, straight from the ranges (rs_mc.cuh), so the layout does not
+// depend on the offsets.
+size_t fast_layout(int R, int W, int NC, KArgs *k) {
     const int WPR = (W + 31) / 32, nwords = R * WPR;
     const int ncw = (NC + 31) / 32;
     int off = 0;
@@ -143,8 +146,8 @@ size_t fast_layout(int R, int W, int n_off, int NC, KArgs *k) {
     o[4] = off; off += nw4;             // NB (run ids before each word)
     o[5] = off; off += wpr4;            // Ph
     o[6] = off; off += wpr4;            // Lh
-    o[7] = off; off += n_off * nwords;  // MC
-    o[8] = off; off += n_off * nwords;  // TL
+    o[7] = off;                         // (MC: none)
+    o[8] = off;                         // (TL: none)
     o[9] = off; off += ncw;             // LR (band-local roots), later kept-word prefixes
     o[10] = off; off += ncw;            // KB (kept roots)
     off = (off + 3) & ~3;
@@ -214,9 +217,9 @@ int make_plan_uncached(const rs_config *cfg, Plan *pl) {
     // fast plan: ~16K cells per band, node capacity from the shared-memory target
     // ~64K cells per band: fewer, larger bands mean fewer cross-band edges and
     // cheaper cluster barriers (measured: 2 bands of 32 rows beat 8 of 8 for
-    // 64x2048 frames).  Many Map Connection bit planes shrink the band until
-    // the run capacity is at least an eighth of its cells (observed: <= 10% for
-    // 32-row bands of the BASELINE configs; more take the overflow path).
+    // 64x2048 frames).  The band shrinks until the run capacity is at least
+    // an eighth of its cells (observed: <= 10% for 32-row bands of the
+    // BASELINE configs; more take the in-kernel overflow path).
     pl->fast = false;
     pl->may_overflow = false;
     pl->smem_f = 0;
@@ -230,7 +233,7 @@ int make_plan_uncached(const rs_config *cfg, Plan *pl) {
         long long lo = 0, hi = cap_full;   // largest capacity under the shared-memory target
         while (lo < hi) {
             const long long mid = (lo + hi + 1) / 2;
-            if (fast_layout(Rf, W, n_off, (int)mid, nullptr) <= kFastSmemTarget) lo = mid; else hi = mid - 1;
+            if (fast_layout(Rf, W, (int)mid, nullptr) <= kFastSmemTarget) lo = mid; else hi = mid - 1;
         }
         long long NC = lo;
         if (cfg->reserved[0] > 0) NC = std::min<long long>(NC, cfg->reserved[0]);   // test hook
@@ -238,15 +241,10 @@ int make_plan_uncached(const rs_config *cfg, Plan *pl) {
         const long long need = std::min<long long>(cap_full, std::max<long long>(kMinNodeCap, (long long)Rf * W / 8));
         if (NC < need && cfg->reserved[0] <= 0) continue;
         NC = std::max<long long>(NC, 32);
-        const size_t smem_f = fast_layout(Rf, W, n_off, (int)NC, nullptr);
+        const size_t smem_f = fast_layout(Rf, W, (int)NC, nullptr);
         if (smem_f > kSmemLimit) continue;
         fill_common(cfg, Rf, pl->kf);
-        fast_layout(Rf, W, n_off, (int)NC, &pl->kf);
-        // Map Connection offsets whose partner row is at most two rows up and
-        // at most 31 columns to the left are tested in step A (registers)
-        for (int o = 0; o < n_off && pl->kf.n_aoff < 4; ++o)
-            if (cfg->offsets[o][0] <= 2 && cfg->offsets[o][1] >= 0 && cfg->offsets[o][1] <= 31)
-                pl->kf.aoff[pl->kf.n_aoff++] = o;
+        fast_layout(Rf, W, (int)NC, &pl->kf);
         pl->kf.NC = (int)NC;
         pl->kf.udyn = pl->kf.C >= RS_UDYN_MIN_C;
         int SHN = 0;
@@ -301,21 +299,16 @@ int set_attrs(const Plan &pl) {
     if (dev != g_attr_device) {
         g_attr_device = dev;
         g_attr_smem_f = g_attr_smem_d = 0;
-        if ((st = cuda_check(cudaFuncSetAttribute(rs::rs_fast_kernel<false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
+        if ((st = cuda_check(cudaFuncSetAttribute(rs::rs_fast_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
                              "cudaFuncSetAttribute(fast, non-portable cluster)")) ||
-            (st = cuda_check(cudaFuncSetAttribute(rs::rs_fast_kernel<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
-                             "cudaFuncSetAttribute(fast/MC, non-portable cluster)")) ||
             (st = cuda_check(cudaFuncSetAttribute(rs::rs_dense_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
                              "cudaFuncSetAttribute(dense, non-portable cluster)")))
             return st;
     }
     if (pl.fast && pl.smem_f > g_attr_smem_f) {
-        if ((st = cuda_check(cudaFuncSetAttribute(rs::rs_fast_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        if ((st = cuda_check(cudaFuncSetAttribute(rs::rs_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                   (int)std::max(pl.smem_f, (size_t)48 * 1024)),
-                             "cudaFuncSetAttribute(fast, smem)")) ||
-            (st = cuda_check(cudaFuncSetAttribute(rs::rs_fast_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                  (int)std::max(pl.smem_f, (size_t)48 * 1024)),
-                             "cudaFuncSetAttribute(fast/MC, smem)")))
+                             "cudaFuncSetAttribute(fast, smem)")))
             return st;
         g_attr_smem_f = pl.smem_f;
     }
@@ -369,10 +362,7 @@ int segment_launch(const Plan &pl, const float *d_tables, const float *d_ranges,
     }
     k.stop_after = pl.stop_after;
     k.planes = d_planes;
-    return k.n_aoff > 0 ? launch_cluster(rs::rs_fast_kernel<true>, k, batch, rs::kFastThreads, pl.smem_f, stream,
-                                         "rs_fast_kernel launch")
-                        : launch_cluster(rs::rs_fast_kernel<false>, k, batch, rs::kFastThreads, pl.smem_f, stream,
-                                         "rs_fast_kernel launch");
+    return launch_cluster(rs::rs_fast_kernel, k, batch, rs::kFastThreads, pl.smem_f, stream, "rs_fast_kernel launch");
 }
 
 // Output checks shared by the device and host entries (before any allocation
@@ -794,6 +784,17 @@ int rs_phase_profile(int64_t *host_out, int32_t max_ctas) {
     return fail(RS_EINVAL, "library built without RS_PHASE_PROF");
 #endif
 }
+
+#ifdef RS_MC_STATS
+int rs_mc_stats(int64_t *host_out, int32_t reset) {
+    int st = cuda_check(cudaMemcpyFromSymbol(host_out, rs::g_mcstats, sizeof(rs::g_mcstats)), "read stats");
+    if (!st && reset) {
+        unsigned long long z[8] = {};
+        st = cuda_check(cudaMemcpyToSymbol(rs::g_mcstats, z, sizeof(z)), "reset stats");
+    }
+    return st;
+}
+#endif
 
 const char *rs_last_error(void) { return g_err.c_str(); }
 

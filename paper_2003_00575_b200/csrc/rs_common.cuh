@@ -39,8 +39,6 @@ struct KArgs {
     int stop_after;               // experiments only (RS_EXPERIMENTS builds): leave the fast kernel after phase N
     uint32_t *planes;             // debug export (rs_fast_planes): the fast kernel's bit planes after step B, or NULL
     int udyn;                     // fast kernel: dynamic edge grabbing in the local unions (clusters of >= 2 bands)
-    int n_aoff;                   // Map Connection offsets evaluated in step A (dy <= 2, 0 <= dx <= 31), at most 4
-    int aoff[4];                  // their indices into dy/dx
 };
 
 // ------------------------------------------------------------ phase markers
@@ -204,6 +202,12 @@ __device__ __forceinline__ int divWPR(const KArgs &a, int w) {
 
 __device__ __forceinline__ uint32_t lanemask_le(int lane) {
     return lane == 31 ? 0xffffffffu : ((2u << lane) - 1u);
+}
+
+// Run id of cell bit b of word w (fast kernel): runs started at or before the
+// cell in this word, plus the runs started before the word.
+__device__ __forceinline__ uint32_t run_of(const uint32_t *SB, const uint32_t *NB, int w, int b) {
+    return NB[w] + __popc(SB[w] & lanemask_le(b)) - 1u;
 }
 
 // ------------------------------------------------------------- TMA staging

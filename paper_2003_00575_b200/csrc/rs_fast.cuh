@@ -34,6 +34,7 @@
 #pragma once
 
 #include "rs_common.cuh"
+#include "rs_mc.cuh"
 #include "rs_overflow.cuh"
 
 namespace rs {
@@ -69,11 +70,6 @@ constexpr int kSweepUnroll = RS_SWEEP_UNROLL;
 constexpr int kFastOcc = RS_FAST_OCC;   // CTAs per SM the fast kernel is sized for
 constexpr int kFastWarps = kFastThreads / 32;
 
-// Run id of cell bit b of word w: runs started at or before the cell in this
-// word, plus the runs started before the word.
-__device__ __forceinline__ uint32_t run_of(const uint32_t *SB, const uint32_t *NB, int w, int b) {
-    return NB[w] + __popc(SB[w] & lanemask_le(b)) - 1u;
-}
 
 struct RunUF {
     uint32_t *E;
@@ -118,6 +114,18 @@ struct RunUF {
             if (x == y) return;
             if (x > y) { const uint32_t t = x; x = y; y = t; }
             const uint32_t old = atomicMin(slot(E, y), x);   // larger root hooks under smaller
+            if (old == y) return;
+            y = old;
+        }
+    }
+    // union of two entries that were roots recently (no hop from a run first)
+    __device__ void unite_roots(uint32_t x, uint32_t y) const {
+        while (true) {
+            x = find(x);
+            y = find(y);
+            if (x == y) return;
+            if (x > y) { const uint32_t t = x; x = y; y = t; }
+            const uint32_t old = atomicMin(slot(E, y), x);
             if (old == y) return;
             y = old;
         }
@@ -179,13 +187,12 @@ struct RunUF {
 // 16-byte stores of the four words by lane 0).  GROUND: ground removal on.
 // Plane stores use 32-bit shared-memory byte addresses (sP/sL/sU: the chunk's
 // words in the band's first row; sPh/sLh: the halo row).
-template <bool FULL, bool MCA, bool GROUND>
+template <bool FULL, bool GROUND>
 struct BitsStrip {
     const KArgs &a;
     const float *col;
     const float *rowc;
     uint32_t sP, sL, sU, sPh, sLh;
-    uint32_t *MCp;
     int ch, lane, r0, rstart, rend, cb;
     float thr, tch;
     int rfirst;   // first row walked (rstart, or a later row when rows are split between warps)
@@ -205,19 +212,13 @@ struct BitsStrip {
     }
 
     // va = row above, v = this row, vb = row below (read by ROW0 only); vn <-
-    // row r + RS_STRIP_SETS - 2 (prefetch; it held row r-2, which MCA reads
-    // first).
+    // row r + RS_STRIP_SETS - 2 (prefetch).
     // Stores the raw ballots: presence P, left pair test EH (in the L plane)
     // and up pair test EV (in the U plane); step B masks them with presence
     // one word per thread, 32x cheaper than warp-uniform ops here.
     template <bool ROW0, bool HALO = false>
     __device__ __forceinline__ void step(int r, const float (&va)[4], const float (&v)[4], const float (&vb)[4],
                                          float (&vn)[4]) const {
-        float v2[4];
-        if (MCA) {
-#pragma unroll
-            for (int j = 0; j < 4; ++j) v2[j] = vn[j];
-        }
         if (!ROW0) ld4(r + RS_STRIP_SETS - 2, vn, r + RS_STRIP_SETS - 2 < rend);
         const float4 c = *reinterpret_cast<const float4 *>(rowc + (r - rstart) * 8);
         const float4 c2 = *reinterpret_cast<const float4 *>(rowc + (r - rstart) * 8 + 4);
@@ -244,33 +245,6 @@ struct BitsStrip {
         }
         const bool halo = HALO;   // only the first row walked in a band > 0 (peeled in run())
         const int cw = ch * 4;
-        if (MCA && !halo) {
-            // raw pair tests of the step-A Map Connection offsets: partner
-            // (r - dy, c - dx) is lane l - dx of word j (or of word j-1 for
-            // l < dx: lanes 32-dx.. send their word j-1 value, as for the left
-            // neighbour); bits l < dx of the chunk's first word and all
-            // presence masking are done in step B
-            for (int i = 0; i < a.n_aoff; ++i) {
-                const int o = a.aoff[i], dy = a.dy[o], dx = a.dx[o];
-                const float tco = __ldg(a.tables + 6 * a.H - 5 + o * a.H + max(r - dy, 0));
-                const int sl = (lane - dx) & 31;
-                const bool prevw = lane >= 32 - dx;
-                uint32_t mw[4];
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const float cur = dy == 0 ? v[j] : dy == 1 ? va[j] : v2[j];
-                    const float prv = j == 0 ? 0.f : (dy == 0 ? v[j > 0 ? j - 1 : 0] : dy == 1 ? va[j > 0 ? j - 1 : 0] : v2[j > 0 ? j - 1 : 0]);
-                    const float pv = __shfl_sync(kFull, (dx > 0 && prevw) ? prv : cur, sl);
-                    mw[j] = __ballot_sync(kFull, pair_pass(pv, v[j], tco, thr));
-                }
-                uint32_t *M = MCp + o * a.nwords + (r - r0) * a.WPR + cw;
-                if (FULL) {
-                    if (lane == 0) *reinterpret_cast<uint4 *>(M) = make_uint4(mw[0], mw[1], mw[2], mw[3]);
-                } else if (lane < 4 && cw + lane < a.WPR) {
-                    M[lane] = lane == 0 ? mw[0] : lane == 1 ? mw[1] : lane == 2 ? mw[2] : mw[3];
-                }
-            }
-        }
         const uint32_t off = halo ? 0u : (uint32_t)((r - r0) * wpb);
         if (FULL) {
             if (lane == 0) {
@@ -318,8 +292,6 @@ struct BitsStrip {
                 S1[j] = S2[j];
                 S2[j] = t;
             }
-        } else if (MCA && rf >= 2) {
-            ld4(rf - 2, S2);   // row r-2 of the first step (Map Connections)
         }
         for (int r = rf; r < rend; r += 3) {
             step<false>(r, S0, S1, S1, S2);
@@ -361,8 +333,6 @@ struct BitsStrip {
                 S2[j] = S3[j];
                 S3[j] = t;
             }
-        } else if (MCA && rf >= 2) {
-            ld4(rf - 2, S3);   // row r-2 of the first step (Map Connections)
         }
         for (int r = rf; r < rend; r += 4) {
             step<false>(r, S0, S1, S2, S3);
@@ -377,10 +347,6 @@ struct BitsStrip {
 #endif
 };
 
-// MCA: some Map Connection offsets (dy <= 2, 0 <= dx <= 31) are tested in
-// step A from the rows already in registers (a separate instantiation, so the
-// default kernel's code is untouched).
-template <bool MCA>
 __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const __grid_constant__ KArgs a) {
     extern __shared__ __align__(128) uint32_t sm[];
     __shared__ uint32_t warp_tot[kFastWarps];
@@ -407,7 +373,6 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
     uint32_t *P = sm + a.o_P, *L = sm + a.o_L, *U = sm + a.o_U;
     uint32_t *SB = sm + a.o_SB, *NB = sm + a.o_RS;
     uint32_t *Ph = sm + a.o_Ph, *Lh = sm + a.o_Lh;
-    uint32_t *MC = sm + a.o_MC, *TL = sm + a.o_TL;
     uint32_t *LR = sm + a.o_LR, *KB = sm + a.o_K;
     uint32_t *E = sm + a.o_E, *SZ = sm + a.o_SZ;
     auto G = [&](int r, int c) -> float { return __ldg(fr + (size_t)r * W + c); };
@@ -449,7 +414,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
             const bool full = ch * 128 + 128 <= W && (WPR & 3) == 0;
 #define RS_STRIP(F, G)                                                                                          \
     do {                                                                                                    \
-        const BitsStrip<F, MCA, G> st{a, fr + cb, rowc, sP, sL, sU, sPh, sLh, MC, ch, lane, r0, rstart, rhi, cb, thr, \
+        const BitsStrip<F, G> st{a, fr + cb, rowc, sP, sL, sU, sPh, sLh, ch, lane, r0, rstart, rhi, cb, thr, \
                                       tch, rlo, 4 * W, 4 * WPR};                                            \
         st.run();                                                                                           \
         umx = max(umx, st.mx);                                                                              \
@@ -513,121 +478,13 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
                 atomicOr(&seam[q >> 5], 1u << (q & 31));
         }
     }
-    if (a.n_off > 0) {
-        // Pairs (r-dy, c-dx mod W) <-> (r, c), evaluated by the lower/right cell;
-        // TL = left edge of the partner (redundant-edge test): the partner's L
-        // bit when its row is in the band or the halo row (L final after this
-        // barrier), else tested here.
-        __syncthreads();
-        RS_MARK(21);
-        auto is_aoff = [&](int o) {
-            bool hit = false;
-            if (MCA)
-                for (int i = 0; i < a.n_aoff; ++i) hit |= a.aoff[i] == o;
-            return hit;
-        };
-        if (MCA) {
-            // offsets tested in step A: mask the raw bits with the presence
-            // of both cells, partner left edges from the L plane, and redo the
-            // bits whose partner lies before the chunk (or across the seam);
-            // one word per thread
-            for (int i = 0; i < a.n_aoff; ++i) {
-                const int o = a.aoff[i], dy = a.dy[o], dx = a.dx[o];
-                uint32_t *M = MC + o * a.nwords, *T = TL + o * a.nwords;
-                for (int w = tid; w < nw; w += kFastThreads) {
-                    const int q = divWPR(a, w);
-                    const int cw = w - q * WPR;
-                    const int r = r0 + q, tr = r - dy;
-                    if (tr < r0 - 1 && tr >= 0) continue;   // partner above the halo row: below
-                    if (tr < 0) { M[w] = 0u; T[w] = 0u; continue; }
-                    const uint32_t *Pt = tr >= r0 ? P + (tr - r0) * WPR : Ph;
-                    const uint32_t *Lt = tr >= r0 ? L + (tr - r0) * WPR : Lh;
-                    const uint32_t pw = P[w];
-                    uint32_t pp = Pt[cw], tl = Lt[cw];
-                    if (dx > 0) {
-                        pp <<= dx;
-                        tl <<= dx;
-                        if (cw > 0) { pp |= Pt[cw - 1] >> (32 - dx); tl |= Lt[cw - 1] >> (32 - dx); }
-                    }
-                    uint32_t m = M[w] & pw & pp;
-                    if (dx > 0 && (cw & 3) == 0) {
-                        const uint32_t low = dx >= 32 ? kFull : ((1u << dx) - 1u);
-                        m &= ~low;
-                        tl &= ~low;
-                        const float tco = __ldg(a.tables + 6 * H - 5 + o * H + tr);
-                        for (int b = 0; b < dx && b < 32; ++b) {
-                            const int c = cw * 32 + b;
-                            if (c >= W) break;
-                            int tc = (c - dx) % W;
-                            if (tc < 0) tc += W;
-                            if ((Lt[tc >> 5] >> (tc & 31)) & 1u) tl |= 1u << b;
-                            if (((pw >> b) & 1u) && ((Pt[tc >> 5] >> (tc & 31)) & 1u) &&
-                                pair_pass(G(tr, tc), G(r, c), tco, thr))
-                                m |= 1u << b;
-                        }
-                    }
-                    M[w] = m;
-                    T[w] = tl;
-                }
-            }
-        }
-        RS_MARK(22);
-        // the per-lane path: every word for offsets not done in step A, and
-        // for those only the first dy-1 rows (partner above the halo row)
-        int wend = MCA ? 0 : nw;
-        for (int o = 0; o < a.n_off && wend < nw; ++o)
-            wend = max(wend, is_aoff(o) ? min(max(a.dy[o] - 1, 0), rows) * WPR : nw);
-        for (int w = warp; w < wend; w += kFastWarps) {
-            const int q = divWPR(a, w);
-            const int cw = w - q * WPR;
-            const int c = cw * 32 + lane;
-            const bool inb = c < W;
-            const int r = r0 + q;
-            const bool p = inb && ((P[w] >> lane) & 1u);
-            float v = 0.f;
-            bool vload = false;
-            for (int o = 0; o < a.n_off; ++o) {
-                const int tr = r - a.dy[o];   // warp-uniform
-                if (is_aoff(o) && !(tr < r0 - 1 && tr >= 0)) continue;   // done above
-                if (!vload) { v = inb ? G(r, c) : 0.f; vload = true; }
-                int tc = (c - a.dx[o]) % W;
-                if (tc < 0) tc += W;
-                const bool has = inb && tr >= 0;
-                const float tco = __ldg(a.tables + 6 * H - 5 + o * H + max(tr, 0));
-                bool mc = false, tl = false;
-                if (tr >= r0 - 1) {
-                    const uint32_t *Pt = tr >= r0 ? P + (tr - r0) * WPR : Ph;
-                    const uint32_t *Lt = tr >= r0 ? L + (tr - r0) * WPR : Lh;
-                    if (has) {
-                        const bool pt = (Pt[tc >> 5] >> (tc & 31)) & 1u;
-                        mc = p && pt && pair_pass(G(tr, tc), v, tco, thr);
-                        tl = (Lt[tc >> 5] >> (tc & 31)) & 1u;
-                    }
-                } else {
-                    bool pt = false, ptl = false;
-                    float vt = 0.f, vtl = 0.f;
-                    if (has) { vt = G(tr, tc); pt = present_at(a, tr, tc, G); }
-                    ptl = __shfl_up_sync(kFull, pt, 1);
-                    vtl = __shfl_up_sync(kFull, vt, 1);
-                    if (has && tc > 0 && c > 0 && lane == 0) { vtl = G(tr, tc - 1); ptl = present_at(a, tr, tc - 1, G); }
-                    mc = has && p && pt && pair_pass(vt, v, tco, thr);
-                    tl = has && c > 0 && tc > 0 && pt && ptl && pair_pass(vtl, vt, tch, thr);
-                }
-                const uint32_t mm = __ballot_sync(kFull, mc);
-                const uint32_t mt = __ballot_sync(kFull, tl);
-                if (lane == 0) {
-                    MC[o * a.nwords + w] = mm;
-                    TL[o * a.nwords + w] = mt;
-                }
-            }
-        }
-    }
     __syncthreads();
     RS_MARK(2);
 #ifndef RS_NO_PLANES
     if (a.planes) {
-        // debug export (rs_fast_planes): P, L (bit 0 of a row = the seam edge),
-        // U and the Map Connection planes of the band's own rows, final here
+        // debug export (rs_fast_planes): P, L (bit 0 of a row = the seam edge)
+        // and U of the band's own rows, final here (the Map Connection planes
+        // are written by the Map Connection pass, mc_pass)
         const size_t fw = (size_t)H * WPR;
         uint32_t *out = a.planes + (size_t)frame * (3 + a.n_off) * fw + (size_t)r0 * WPR;
         for (int w = tid; w < nw; w += kFastThreads) {
@@ -636,7 +493,6 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
             out[w] = P[w];
             out[fw + w] = L[w] | (sm0 ? 1u : 0u);
             out[2 * fw + w] = U[w];
-            for (int o = 0; o < a.n_off; ++o) out[(3 + o) * fw + w] = MC[o * a.nwords + w];
         }
     }
 #endif
@@ -716,14 +572,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
                     nru = uw & ~(uprev & lw & L[w - WPR]);
                 }
                 const bool sm_ = act && cw == 0 && ((seam[q >> 5] >> (q & 31)) & 1u);
-                uint32_t k = (uint32_t)pseudo + __popc(nru) + (uint32_t)sm_;
-                for (int o = 0; o < a.n_off && act; ++o) {
-                    if (q < a.dy[o]) continue;   // partner above the band: step X
-                    const uint32_t *M = MC + o * a.nwords;
-                    const uint32_t m = M[w];
-                    const uint32_t mprev = (m << 1) | (cw > 0 ? M[w - 1] >> 31 : 0u);
-                    k += __popc(m & ~(mprev & lw & TL[o * a.nwords + w]));
-                }
+                const uint32_t k = (uint32_t)pseudo + __popc(nru) + (uint32_t)sm_;
                 uint32_t slot = 0;
                 if (!direct && __any_sync(kFull, k != 0u)) {
                     // warp-aggregated reservation in the edge list
@@ -756,19 +605,6 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
                     }
                 }
                 if (sm_) push(x0, run_of(SB, NB, q * WPR + (W - 1) / 32, (W - 1) & 31));
-                for (int o = 0; o < a.n_off; ++o) {
-                    const int dy = a.dy[o];
-                    if (q < dy) continue;
-                    const uint32_t *M = MC + o * a.nwords;
-                    const uint32_t m = M[w];
-                    const uint32_t mprev = (m << 1) | (cw > 0 ? M[w - 1] >> 31 : 0u);
-                    for (uint32_t nr = m & ~(mprev & lw & TL[o * a.nwords + w]); nr; nr &= nr - 1) {
-                        const int b = __ffs(nr) - 1;
-                        int tc = (cw * 32 + b - a.dx[o]) % W;
-                        if (tc < 0) tc += W;
-                        push(run_of(SB, NB, w, b), run_of(SB, NB, (q - dy) * WPR + tc / 32, tc & 31));
-                    }
-                }
             }
         };
         gather(false);
@@ -886,7 +722,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
     }
     __syncthreads();
     if (ovf_any) {   // cluster-uniform: union-find over cells in global memory (rs_overflow.cuh)
-        overflow_frame(a, P, L, U, Lh, MC, seam, ovf_cnt, warp_tot, frame, &cta_bad);
+        overflow_frame(a, P, L, U, Lh, seam, ovf_cnt, warp_tot, frame, &cta_bad);
         return;
     }
 
@@ -943,38 +779,73 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
         const int whalf = WPR / 2;
         if (r0 > 0) boundary(k, whalf, WPR);
         if (k + 1 < a.C) boundary(k + 1, 0, whalf);
-        if (r0 > 0) {
-            for (int o = 0; o < a.n_off; ++o) {
-                const int dy = a.dy[o];
-                const uint32_t *M = MC + o * a.nwords, *T = TL + o * a.nwords;
-                for (int q = 0; q < min(dy, rows); ++q) {
-                    const int tr = r0 + q - dy;
-                    if (tr < 0) continue;
-                    const int kt = tr / R, tq = tr - kt * R;
-                    const uint32_t *SBt = cl.map_shared_rank(SB, kt), *NBt = cl.map_shared_rank(NB, kt);
-                    for (int cbase = warp * 32; cbase < WPR * 32; cbase += kFastThreads) {
-                        const int c = cbase + lane;
-                        const int cw = c >> 5, b = c & 31, w = q * WPR + cw;
-                        const uint32_t m = M[w];
-                        const uint32_t mpb = b > 0 ? (m >> (b - 1)) & 1u : (cw > 0 ? M[w - 1] >> 31 : 0u);
-                        const bool has =
-                            c < W && ((m >> b) & 1u) && !(mpb && ((L[w] >> b) & 1u) && ((T[w] >> b) & 1u));
-                        int tc = (c - a.dx[o]) % W;
-                        if (tc < 0) tc += W;
-                        xpush(has, has ? band | run_of(SB, NB, w, b) : 0u,
-                              has ? ((uint32_t)kt << a.SHN) | run_of(SBt, NBt, tq * WPR + tc / 32, tc & 31) : 0u);
-                    }
-                }
-            }
-        }
         __syncthreads();
         const uint32_t nx = min(n_xedges, xcap);
         for (uint32_t e = tid; e < nx; e += kFastThreads) uf.unite(XL[2 * e], XL[2 * e + 1]);
     }
     RS_STOP(5);
     RS_MARK(8);
-    cl.sync();   // #2: the forest is final
+    cl.sync();   // #2: the forest of the direct edges is final
     RS_MARK(9);
+#ifndef RS_MC_NO_PASS
+    if (a.n_off > 0) {
+        // ---- M. Map Connection edges (rs_mc.cuh).  Every run first points
+        // straight at its root (a compression of the final direct-edge forest;
+        // other bands may still be compressing, which only makes a root
+        // comparison say "different" more often), then pairs whose chains
+        // join different roots are tested; passing ones are listed in the U
+        // plane (free: the cross-band list is consumed) and united by all
+        // threads.  Step L then takes two hops (run -> old root -> final root).
+        for (uint32_t id = tid; id < n_runs; id += kFastThreads) E[id] = uf.find_nc(band | id);
+        if (tid == 0) n_edges = 0;
+        __syncthreads();
+        RS_MARK(21);
+        uint32_t *ML = U;
+        const uint32_t mcap = (uint32_t)(nw / 2);
+        uint32_t *exp = a.planes ? a.planes + (size_t)frame * (3 + a.n_off) * H * WPR : nullptr;
+        auto run_in = [&](int kt, int tw, int tb) {
+            const uint32_t *SBt = kt == k ? SB : cl.map_shared_rank(SB, kt);
+            const uint32_t *NBt = kt == k ? NB : cl.map_shared_rank(NB, kt);
+            return ((uint32_t)kt << a.SHN) | run_of(SBt, NBt, tw, tb);
+        };
+        if (!exp)
+            mc_runs(a, cl, k, P, L, SB, NB, fr, r0, rows, n_runs, tid, kFastThreads, ML, mcap, &ucur,
+                    [&](int kt, uint32_t id) { return kt == k ? E[id] : *cl.map_shared_rank(E + id, kt); },
+                    [&](int kt, uint32_t id) { return uf.find_nc(((uint32_t)kt << a.SHN) | id); },
+                    [&](uint32_t x, uint32_t y) { uf.unite_roots(x, y); });
+        else   // parity export: every present pair tested and its decision written
+        mc_pass<true>(
+            a, cl, k, P, L, fr, r0, rows, lane, warp, kFastWarps, exp,
+            [&](int w, int b) { return E[run_of(SB, NB, w, b)]; },
+            [&](int kt, int tw, int tb) { return uf.ld(run_in(kt, tw, tb)); },
+            [&](bool has, int w, int b, int kt, int tw, int, int, int, int tc) {
+                uint32_t x = 0, y = 0;
+                if (has) {
+                    x = band | run_of(SB, NB, w, b);
+                    y = run_in(kt, tw, tc & 31);
+                }
+                const uint32_t m = __ballot_sync(kFull, has);
+                if (!m) return;
+                uint32_t base = 0;
+                if (lane == 0) base = atomicAdd(&n_edges, (uint32_t)__popc(m));
+                base = __shfl_sync(kFull, base, 0);
+                if (!has) return;
+                const uint32_t slot = base + __popc(m & ((1u << lane) - 1u));
+                if (slot < mcap) {
+                    ML[2 * slot] = x;
+                    ML[2 * slot + 1] = y;
+                } else {
+                    uf.unite(x, y);
+                }
+            });
+        __syncthreads();
+        RS_MARK(22);
+        const uint32_t nm = min(n_edges, mcap);
+        for (uint32_t e = tid; e < nm; e += kFastThreads) uf.unite(ML[2 * e], ML[2 * e + 1]);
+        RS_MARK(23);
+        cl.sync();   // #2b: Map Connection unions done
+    }
+#endif
 
     // ---- Z. resolve: local roots chase their global root and add their size ---
     // Only band-local roots move (E[lr] = global root); other runs keep their
@@ -1072,7 +943,10 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
 #pragma unroll 4
         for (uint32_t id = tid; id < n_runs; id += kFastThreads) {
             const uint32_t lr = E[id];
-            const uint32_t g = ((lr >> a.SHN) == (uint32_t)k) ? E[lr & maskN] : lr;
+            // lr: the band-local root (E[lr] = the final root after Z), or
+            // with Map Connections the root before step M (a local root of
+            // its band: one hop, possibly over DSMEM, to the final root)
+            const uint32_t g = ((lr >> a.SHN) == (uint32_t)k) ? E[lr & maskN] : (a.n_off ? uf.ld(lr) : lr);
             const int owner = (int)(g >> a.SHN);
             const uint32_t gi = g & maskN;
             uint32_t km, wk;

@@ -1,0 +1,281 @@
+// rs_mc.cuh — Map Connections (map_connections.py:132-178) in the fused
+// kernel, as extra edges of the component graph.
+//
+// The reference labels the frame first, then for every offset (dy, dx) tests
+// the pairs (r, c) - (r + dy, (c + dx) mod W) whose labels are > 0 and differ
+// (pair_distance_sq with the pair's upper-row constant, :155-169) and unions
+// their clusters (ClusterUnion, :73-110); filter_small runs on the merged
+// clusters.  The result is the connected components of the graph (present
+// cells; direct edges plus every passing Map Connection pair).
+//
+// The fused kernel does the same once its direct-edge forest is final
+// (barrier #2) and every run points straight at its root: a pair is tested
+// only if its two cells have different roots — the reference's "labels
+// differ".  Pairs come in chains: along a row, consecutive candidate pairs
+// whose own cells and partner cells are left-linked join the same two runs,
+// so the roots are compared once per chain (at its head) and the verdict is
+// shared along the chain.  Most chains lie inside one component, so few
+// ranges are loaded at all; passing pairs go into the same cluster-wide
+// union-find as the other edges.  Presence and left-link bits of the partner
+// row are built a word at a time (a funnel shift of two plane words, local or
+// over DSMEM).  No per-offset bit plane is kept in shared memory, so the band
+// layout (and the two-CTAs-per-SM occupancy) is the same with any number of
+// offsets.
+//
+// With `out` set (rs_fast_planes), or without ROOTS (the overflow path),
+// every present pair is tested; `out` then receives the decision words as
+// plane 3 + o of the frame.
+#pragma once
+
+#include "rs_common.cuh"
+
+namespace rs {
+
+// The 32 bits of plane row `row` (W cells, WPR words) starting at cell t0
+// (wrapping at W; W % 32 == 0 for the funnel path).
+__device__ __forceinline__ uint32_t row_bits(const uint32_t *row, int t0, int W, int WPR, int lane, bool funnel) {
+    if (funnel) {
+        const int a = t0 >> 5, sh = t0 & 31;
+        const uint32_t lo = row[a], hi = row[a + 1 == WPR ? 0 : a + 1];
+        return sh ? __funnelshift_r(lo, hi, sh) : lo;
+    }
+    const int t = (t0 + lane) % W;
+    return __ballot_sync(kFull, (row[t >> 5] >> (t & 31)) & 1u);
+}
+
+// root_own(w, b) / root_partner(kt, tw, tb): root of the own cell (word w,
+// bit b) / of the partner cell (band kt, word tw of that band, bit tb); only
+// called when ROOTS.  edge(has, w, b, kt, tw, r, c, tr, tc) is called by
+// EVERY lane of the warp (warp-synchronous; `has` marks a lane with an edge).
+template <bool ROOTS, class RootOwn, class RootPartner, class Edge>
+__device__ __forceinline__ void mc_pass(const KArgs &a, const cg::cluster_group &cl, int k, const uint32_t *P,
+                                        const uint32_t *L, const float *fr, int r0, int rows, int lane, int warp,
+                                        int nwarps, uint32_t *out, RootOwn root_own, RootPartner root_partner,
+                                        Edge edge) {
+    const int H = a.H, W = a.W, R = a.R, WPR = a.WPR;
+    const size_t fw = (size_t)H * WPR;
+    const float thr = a.dmax2;
+    const bool filter = ROOTS && out == nullptr;
+    const bool funnel = (W & 31) == 0;
+    const uint32_t below = (1u << lane) - 1u;
+    for (int q = warp; q < rows; q += nwarps) {
+        const int r = r0 + q;
+        for (int o = 0; o < a.n_off; ++o) {
+            const int tr = r - a.dy[o];
+            if (tr < 0) {
+                if (out && lane == 0)
+                    for (int cw = 0; cw < WPR; ++cw) out[(size_t)(3 + o) * fw + (size_t)r * WPR + cw] = 0u;
+                continue;
+            }
+            const int dx = a.dx[o];
+            const int kt = tr / R, tq = tr - kt * R;
+            const uint32_t *Pt = (kt == k ? P : cl.map_shared_rank(P, kt)) + tq * WPR;
+            const uint32_t *Lt = (kt == k ? L : cl.map_shared_rank(L, kt)) + tq * WPR;
+            const float tco = __ldg(a.tables + 6 * H - 5 + o * H + tr);
+            const float *trow = fr + (size_t)tr * W, *orow = fr + (size_t)r * W;
+            int t0 = -dx % W;   // partner of column 0
+            t0 = t0 < 0 ? t0 + W : t0;
+            uint32_t ccand = 0, cdiff = 0, cm = 0;   // lane 31's candidate / chain verdict / decision, previous word
+            for (int cw = 0; cw < WPR; ++cw, t0 = (t0 + 32 >= W ? t0 + 32 - W : t0 + 32)) {
+                const int w = q * WPR + cw;
+                const uint32_t pw = P[w];
+                const uint32_t cand = pw ? pw & row_bits(Pt, t0, W, WPR, lane, funnel) : 0u;   // warp-uniform
+                if (!cand) {
+                    ccand = cdiff = cm = 0;
+                    if (out && lane == 0) out[(size_t)(3 + o) * fw + (size_t)r * WPR + cw] = 0u;
+                    continue;
+                }
+                const uint32_t lw = L[w], ltw = row_bits(Lt, t0, W, WPR, lane, funnel);
+                // chain continuation: the left neighbours are a candidate pair and both cells are left-linked to them
+                const uint32_t chain = cand & ((cand << 1) | ccand) & lw & ltw;
+                const uint32_t heads = cand & ~chain;
+                int tc = t0 + lane;
+                tc = funnel ? (tc >= W ? tc - W : tc) : tc % W;
+                const int tw = tq * WPR + (tc >> 5);
+                const bool mine = (cand >> lane) & 1u;
+                bool diff = mine;
+                if (filter) {
+                    bool hd = false;
+                    if ((heads >> lane) & 1u) hd = root_own(w, lane) != root_partner(kt, tw, tc & 31);
+                    const uint32_t D = __ballot_sync(kFull, hd);
+                    const uint32_t hb = heads & (below | (1u << lane));   // heads at or below this lane
+                    diff = mine && (hb ? (D >> (31 - __clz(hb))) & 1u : cdiff);
+                }
+                bool mc = false;
+                if (__any_sync(kFull, diff) && diff)
+                    mc = pair_pass(__ldg(trow + tc), __ldg(orow + min(cw * 32 + lane, W - 1)), tco, thr);
+                const uint32_t m = __ballot_sync(kFull, mc);
+                // the left neighbours' pair passed and links both cells to this pair's runs: nothing new
+                const bool prev = lane > 0 ? (m >> (lane - 1)) & 1u : cm;
+                const bool has = mc && !(prev && ((chain >> lane) & 1u));
+                edge(has, w, lane, kt, tw, r, cw * 32 + lane, tr, tc);
+                if (out && lane == 0) out[(size_t)(3 + o) * fw + (size_t)r * WPR + cw] = m;
+                ccand = cand >> 31;
+                cdiff = __shfl_sync(kFull, (uint32_t)diff, 31);
+                cm = m >> 31;
+            }
+        }
+    }
+}
+
+}  // namespace rs
+
+namespace rs {
+
+#ifdef RS_MC_STATS
+__device__ unsigned long long g_mcstats[8];
+#define RS_MCSTAT(i, v) atomicAdd(&g_mcstats[i], (unsigned long long)(v))
+#else
+#define RS_MCSTAT(i, v) \
+    do {                \
+    } while (0)
+#endif
+
+// Run end: the last cell of the run starting at bit b of word cw of a row
+// (left links continuing after it).
+__device__ __forceinline__ int run_end(const uint32_t *Lrow, int cw, int b, int WPR, int W) {
+    const uint32_t y = b < 31 ? Lrow[cw] >> (b + 1) : 0u;
+    const int n = __ffs(~y) - 1;   // consecutive links (<= 31 - b)
+    int e;
+    if (n < 31 - b) {
+        e = cw * 32 + b + n;
+    } else {
+        e = cw * 32 + 31;
+        for (int ww = cw + 1; ww < WPR; ++ww) {
+            const uint32_t m = ~Lrow[ww];
+            if (m) { e = ww * 32 + __ffs(m) - 2; break; }
+            e = ww * 32 + 31;
+        }
+    }
+    return min(e, W - 1);
+}
+
+// Map Connections over RUNS (the production path of the fast kernel; the
+// cell-level mc_pass above serves the parity export and the overflow path).
+// Called by every thread of the CTA (it synchronises the CTA).
+//
+// One round per offset.  Thread i takes runs i, i + nthreads, ... of the band
+// (ids follow cell order: the word holding the j-th start is found by a
+// binary search of the per-word run counts NB, the bit by __fns), so every
+// lane has a run and the loop is uniform.  For the run [s, e] of row r the
+// partner cells are the segment [s - dx, e - dx] (mod W) of row r - dy, and
+// the partner runs overlapping it are a contiguous range of run ids.  Each is
+// compared with the own run by root in the forest's compressed snapshot; a
+// differing pair (the reference's "labels differ") is listed.  Then every
+// thread takes a listed pair: if the live forest still has them apart (an
+// earlier union may have joined them) the aligned cells are tested until one
+// passes, and the runs are united.  Step R's pseudo starts (a run continuing
+// into a warp's word range gets a second id there; both ids have one root) are
+// skipped as own runs: the run is walked from its true start through them.
+//
+// Callbacks: root(kt, id) = snapshot root of run `id` of band kt (one load);
+// live(kt, id) = its root in the live forest (a find); unite(x, y) joins two
+// (possibly no longer) roots of the live forest.  list / cap / count: a buffer of 2 * cap
+// words and a shared counter.
+template <class Root, class Live, class Unite>
+__device__ __forceinline__ void mc_runs(const KArgs &a, const cg::cluster_group &cl, int k, const uint32_t *P,
+                                        const uint32_t *L, const uint32_t *SB, const uint32_t *NB, const float *fr,
+                                        int r0, int rows, uint32_t n_runs, int tid, int nthreads, uint32_t *list,
+                                        uint32_t cap, uint32_t *count, Root root, Live live, Unite unite) {
+    const int H = a.H, W = a.W, R = a.R, WPR = a.WPR;
+    const float thr = a.dmax2;
+    const int nw = rows * WPR;
+    // test the pair (own run starting at band cell sc, run j of band kt) and unite on a pass
+    auto resolve = [&](int o, uint32_t own, int kt, uint32_t j, int sc, int part) {
+#ifdef RS_MC_NOLIVE
+        return;
+#endif
+        const uint32_t lx = live(k, own), ly = live(kt, j);
+        if (lx == ly) return;
+#ifdef RS_MC_NOSLOW
+        return;
+#endif
+        const int q = sc / W, s = sc - q * W, r = r0 + q;
+        const int e = run_end(L + q * WPR, s >> 5, s & 31, WPR, W);
+        const int dy = a.dy[o], dx = a.dx[o], tr = r - dy;
+        const int tq = tr - kt * R;
+        const uint32_t *Pt = (kt == k ? P : cl.map_shared_rank(P, kt)) + tq * WPR;
+        const uint32_t *SBt = kt == k ? SB : cl.map_shared_rank(SB, kt);
+        const uint32_t *NBt = kt == k ? NB : cl.map_shared_rank(NB, kt);
+        int t0 = (s - dx) % W;
+        t0 = t0 < 0 ? t0 + W : t0;
+        const int len = e - s;
+        const int a0 = part ? 0 : t0, a1 = part ? t0 + len - W : min(t0 + len, W - 1);
+        const float tco = __ldg(a.tables + 6 * H - 5 + o * H + tr);
+        RS_MCSTAT(2, 1);
+        for (int t = a0; t <= a1; ++t) {
+            if (!((Pt[t >> 5] >> (t & 31)) & 1u) || run_of(SBt, NBt, tq * WPR + (t >> 5), t & 31) != j) continue;
+            const int c = s + (t - a0) + (part ? (W - t0) : 0);
+            RS_MCSTAT(3, 1);
+            if (pair_pass(__ldg(fr + (size_t)tr * W + t), __ldg(fr + (size_t)r * W + c), tco, thr)) {
+#ifndef RS_MC_NOUNITE
+                unite(lx, ly);   // from the live roots: no finds from the runs again
+#endif
+                RS_MCSTAT(4, 1);
+                return;
+            }
+        }
+    };
+    for (int o = 0; o < a.n_off; ++o) {
+        if (tid == 0) *count = 0;
+        __syncthreads();
+        const int dy = a.dy[o], dx = a.dx[o];
+        for (uint32_t own = tid; own < n_runs; own += nthreads) {
+            int lo = 0, hi = nw - 1;   // the word holding start `own`: the last w with NB[w] <= own
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (NB[mid] <= own) lo = mid; else hi = mid - 1;
+            }
+            const int w = lo;
+            const int b = (int)__fns(SB[w], 0, (int)(own - NB[w]) + 1);
+            if ((L[w] >> b) & 1u) continue;   // pseudo start: walked from the run's true start
+            const int q = divWPR(a, w), cw = w - q * WPR, r = r0 + q;
+            const int tr = r - dy;
+            if (tr < 0) continue;
+            const int s = cw * 32 + b;
+            const int e = run_end(L + q * WPR, cw, b, WPR, W);
+            const uint32_t rown = root(k, own);
+            const int kt = tr / R, tq = tr - kt * R;
+            const uint32_t *Pt = (kt == k ? P : cl.map_shared_rank(P, kt)) + tq * WPR;
+            const uint32_t *SBt = kt == k ? SB : cl.map_shared_rank(SB, kt);
+            const uint32_t *NBt = kt == k ? NB : cl.map_shared_rank(NB, kt);
+            auto rid = [&](int t) { return run_of(SBt, NBt, tq * WPR + (t >> 5), t & 31); };
+            RS_MCSTAT(0, 1);
+            int t0 = (s - dx) % W;
+            t0 = t0 < 0 ? t0 + W : t0;
+            const int len = e - s;
+            for (int part = 0; part < 2; ++part) {   // the partner segment, split at the seam
+                if (part == 1 && t0 + len < W) break;
+                const int a0 = part ? 0 : t0, a1 = part ? t0 + len - W : min(t0 + len, W - 1);
+                const uint32_t j0 = rid(a0) + (((Pt[a0 >> 5] >> (a0 & 31)) & 1u) ? 0u : 1u);
+                const uint32_t j1 = rid(a1);
+                if (j1 + 1u == 0u || j0 > j1) continue;   // no partner run in the segment
+                for (uint32_t j = j0; j <= j1; ++j) {
+                    RS_MCSTAT(1, 1);
+                    if (root(kt, j) == rown) continue;
+                    // list slot: one shared atomic per group of lanes pushing together
+                    const uint32_t am = __activemask();
+                    const int leader = __ffs(am) - 1, lane = threadIdx.x & 31;
+                    uint32_t base = 0;
+                    if (lane == leader) base = atomicAdd(count, (uint32_t)__popc(am));
+                    const uint32_t slot = __shfl_sync(am, base, leader) + __popc(am & ((1u << lane) - 1u));
+                    if (slot < cap) {
+                        list[2 * slot] = own | ((uint32_t)kt << 16) | ((uint32_t)part << 20);
+                        list[2 * slot + 1] = j | ((uint32_t)(q * W + s) << 16);
+                    } else {
+                        resolve(o, own, kt, j, q * W + s, part);   // list full: at once
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        const uint32_t n = min(*count, cap);
+        for (uint32_t i = tid; i < n; i += nthreads) {
+            const uint32_t x = list[2 * i], y = list[2 * i + 1];
+            resolve(o, x & 0xffffu, (int)((x >> 16) & 15u), y & 0xffffu, (int)(y >> 16), (int)(x >> 20) & 1);
+        }
+        __syncthreads();
+    }
+}
+
+}  // namespace rs

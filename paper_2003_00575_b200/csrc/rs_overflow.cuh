@@ -1,8 +1,8 @@
 // rs_overflow.cuh — in-kernel fallback of rs_fast_kernel for a frame whose
 // run count exceeds the shared-memory node capacity of some band.
 //
-// The cluster keeps its bit planes (presence P, left edges L, up edges U, Map
-// Connection edges MC, seam bits: all final after step B) and runs a
+// The cluster keeps its bit planes (presence P, left edges L, up edges U, seam
+// bits: all final after step B) and runs a
 // union-find over CELLS in global memory, with the frame's own label buffer
 // as the parent array (no workspace).  It reproduces the same closed form as
 // the fast path (SURVEY.md finding 2): the root of a component is its
@@ -24,6 +24,7 @@
 #pragma once
 
 #include "rs_common.cuh"
+#include "rs_mc.cuh"
 
 namespace rs {
 
@@ -81,14 +82,14 @@ __device__ __forceinline__ void ovf_unite(int *par, int x, int y) {
 }
 
 // Called by every thread of every CTA of the cluster (cluster-uniform branch).
-// P/L/U/MC: this band's planes (shared memory); Lh: the halo row's left
+// P/L/U: this band's planes (shared memory); Lh: the halo row's left
 // edges; seamw: this band's seam bits; cnt: two shared words of this CTA
 // published to the cluster; wtot: one shared word per warp.
 //
 // Passes walk the band word by word, a warp per word and a lane per cell, so
 // every global access of a warp is one coalesced 128-byte row segment.
 __device__ RS_OVF_INLINE void overflow_frame(const KArgs &a, const uint32_t *P, const uint32_t *L, const uint32_t *U,
-                                             const uint32_t *Lh, const uint32_t *MC, const uint32_t *seamw, uint32_t *cnt,
+                                             const uint32_t *Lh, const uint32_t *seamw, uint32_t *cnt,
                                              uint32_t *wtot, int frame, const uint32_t *bad) {
     cg::cluster_group cl = cg::this_cluster();
     const int k = (int)cl.block_rank();
@@ -115,7 +116,8 @@ __device__ RS_OVF_INLINE void overflow_frame(const KArgs &a, const uint32_t *P, 
     }
     cl.sync();
     // F2: unite along the up edges that the left neighbour's up edge does not
-    // already imply, the seam and the Map Connection edges
+    // already imply, the seam and the Map Connection edges (tested here from
+    // the ranges, rs_mc.cuh)
     for (int w = warp; w < rows * WPR; w += nwarp) {
         const int q = w / WPR, cw = w - q * WPR, c = cw * 32 + lane;
         const int g = g0 + q * W + c, r = r0 + q;
@@ -126,12 +128,14 @@ __device__ RS_OVF_INLINE void overflow_frame(const KArgs &a, const uint32_t *P, 
             if (((uw & ~(uprev & lw & la)) >> lane) & 1u) ovf_unite(par, g, g - W);
         }
         if (cw == 0 && lane == 0 && W > 1 && ((seamw[q >> 5] >> (q & 31)) & 1u)) ovf_unite(par, g, r * W + W - 1);
-        for (int o = 0; o < a.n_off; ++o) {
-            if (!((MC[o * a.nwords + w] >> lane) & 1u)) continue;
-            int tc = (c - a.dx[o]) % W;
-            if (tc < 0) tc += W;
-            ovf_unite(par, g, (r - a.dy[o]) * W + tc);
-        }
+    }
+    if (a.n_off > 0) {   // Map Connection edges (rs_mc.cuh)
+        uint32_t *exp = a.planes ? a.planes + (size_t)frame * (3 + a.n_off) * H * WPR : nullptr;
+        mc_pass<false>(a, cl, k, P, L, a.ranges + (size_t)frame * H * W, r0, rows, lane, warp, nwarp, exp,
+                       [](int, int) { return 0u; }, [](int, int, int) { return 0u; },
+                       [&](bool has, int, int, int, int, int r, int c, int tr, int tc) {
+                           if (has) ovf_unite(par, r * W + c, tr * W + tc);
+                       });
     }
     cl.sync();
     // F3: flatten.  Only run starts are ever roots or parents (every other

@@ -63,11 +63,11 @@ ok = (buf[:, 19] > 0) & (buf[:, 20] > 0)
 for nm, i, j in sub:
     d2 = (buf[ok, j] - buf[ok, i]).astype(np.float64)
     print(f"  U.{nm:10s} mean {d2.mean():9.0f}  p90 {np.percentile(d2, 90):9.0f}")
-okb = (buf[:, 21] > 0) & (buf[:, 22] > 0)
-if okb.any():
-    for nm, i, j in [("B.edges+seam", 1, 21), ("B.step-A MC", 21, 22), ("B.other MC", 22, 2)]:
+okb = (buf[:, 21] > 0) & (buf[:, 22] > 0) & (buf[:, 23] > 0)
+if okb.any():   # step M (Map Connections) inside "Z resolve"
+    for nm, i, j in [("M.compress", 9, 21), ("M.runs", 21, 22), ("M.list unite", 22, 23), ("M.cs2b+Z", 23, 10)]:
         d3 = (buf[okb, j] - buf[okb, i]).astype(np.float64)
-        print(f"  {nm:14s} mean {d3.mean():9.0f}  p90 {np.percentile(d3, 90):9.0f}")
+        print(f"  {nm:14s} mean {d3.mean():9.0f}  p90 {np.percentile(d3, 90):9.0f}  max {d3.max():9.0f}")
 C = pipe.ctas_per_frame
 if C > 1:
     rank = np.arange(n) % C
