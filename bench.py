@@ -418,6 +418,13 @@ def time_kernel(pipe, frames, labels, ncl, sizes, steps, flush, stream):
     return sum(a.elapsed_time(b) for a, b in ev) / steps
 
 
+def _plan_of(pipe, batch):
+    from paper_2003_00575_b200 import _native
+    d = _native.plan_batch(pipe.rs_config, batch)
+    return {"rows_per_cta": d["fast_rows"] if d["fast"] else d["dense_rows"],
+            "ctas_per_frame": d["fast_ctas"] if d["fast"] else d["dense_ctas"], "fast": bool(d["fast"])}
+
+
 def per_config_block(args, dev, flush, peak):
     """Every BASELINE config (reference defaults) plus the core / skip /
     Map Connection variants: kernel ms per batch, frames/s, roofline fraction
@@ -449,8 +456,7 @@ def per_config_block(args, dev, flush, peak):
              "ms": ms, "frames_per_s": B / (ms * 1e-3), "points_per_s": cells / (ms * 1e-3),
              "bytes_per_cell": bpc, "frac": cells * bpc / (ms * 1e-3) / 1e9 / peak,
              "compulsory_frac": cells * COMPULSORY_BYTES_PER_CELL / (ms * 1e-3) / 1e9 / peak,
-             "plan": {"rows_per_cta": pipe.rows_per_cta, "ctas_per_frame": pipe.ctas_per_frame,
-                      "fast": bool(pipe.plan["fast"])}}
+             "plan": _plan_of(pipe, B)}
         if not args.no_check:
             e.update(parity_check(pipe, frames))
         out[label] = e

@@ -87,14 +87,19 @@ typedef struct rs_config {
 /* Number of floats in the constant-table block. */
 size_t rs_tables_count(int32_t height, int32_t n_offsets);
 
-/* Launch geometry the library would use for cfg (rows per CTA band, CTAs per
- * frame = cluster size, dynamic shared memory per CTA). */
+/* Launch geometry the library would use for cfg on a large batch (rows per
+ * CTA band, CTAs per frame = cluster size, dynamic shared memory per CTA). */
 int rs_plan(const rs_config *cfg, int32_t *rows_per_cta, int32_t *ctas_per_frame,
             size_t *smem_bytes);
 
 /* Plan details: {fast kernel used, overflow possible, fast rows, fast CTAs,
  * fast smem, node capacity, dense rows, dense CTAs, dense smem}. */
 int rs_plan_detail(const rs_config *cfg, int32_t *out, int32_t n);
+
+/* The same for a launch of `batch` frames: a batch that fills fewer than 148
+ * CTAs (one per SM) gets thinner bands, up to a 16-CTA cluster per frame
+ * (batch 0: the large-batch plan, as rs_plan_detail). */
+int rs_plan_batch(const rs_config *cfg, int32_t batch, int32_t *out, int32_t n);
 
 /* B frames, device pointers, enqueued on `stream` (a cudaStream_t; NULL = legacy
  * default stream).  One kernel launch; asynchronous: returns after it.  No

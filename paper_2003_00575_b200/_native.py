@@ -18,7 +18,7 @@ MAX_OFFSETS = 32
 RS_OK, RS_EINVAL, RS_ECUDA, RS_ETOOLARGE, RS_ENODEV = range(5)
 RS_FRAME_INVALID = -1   # n_clusters[b] of a frame that breaks the input contract
 
-EXPORTS = ("rs_tables_count", "rs_plan", "rs_plan_detail",
+EXPORTS = ("rs_tables_count", "rs_plan", "rs_plan_detail", "rs_plan_batch",
            "rs_segment_batch", "rs_segment_batch_host", "rs_fast_planes", "rs_stage_masks", "rs_project",
            "rs_project_workspace_size", "rs_contingency", "rs_contingency_workspace_size",
            "rs_height_image", "rs_ground_mask", "rs_connectivity",
@@ -68,6 +68,9 @@ def lib():
                                        _P, _P, _P, ctypes.c_int64, _P]
         L.rs_fast_planes.restype = ctypes.c_int
         L.rs_fast_planes.argtypes = [ctypes.POINTER(RsConfig), _P, _P, ctypes.c_int32, _P, _P, _P, _P]
+        L.rs_plan_batch.restype = ctypes.c_int
+        L.rs_plan_batch.argtypes = [ctypes.POINTER(RsConfig), ctypes.c_int32, ctypes.POINTER(ctypes.c_int32),
+                                    ctypes.c_int32]
         L.rs_plan_detail.restype = ctypes.c_int
         L.rs_plan_detail.argtypes = [ctypes.POINTER(RsConfig), ctypes.POINTER(ctypes.c_int32),
                                      ctypes.c_int32]
@@ -142,6 +145,13 @@ PLAN_FIELDS = ("fast", "may_overflow", "fast_rows", "fast_ctas", "fast_smem", "n
 def plan_detail(cfg: RsConfig) -> dict:
     out = (ctypes.c_int32 * len(PLAN_FIELDS))()
     check(lib().rs_plan_detail(ctypes.byref(cfg), out, len(PLAN_FIELDS)), "rs_plan_detail")
+    return dict(zip(PLAN_FIELDS, list(out)))
+
+
+def plan_batch(cfg: RsConfig, batch: int) -> dict:
+    """The plan of a launch of ``batch`` frames (small batches get thinner bands)."""
+    out = (ctypes.c_int32 * len(PLAN_FIELDS))()
+    check(lib().rs_plan_batch(ctypes.byref(cfg), int(batch), out, len(PLAN_FIELDS)), "rs_plan_batch")
     return dict(zip(PLAN_FIELDS, list(out)))
 
 

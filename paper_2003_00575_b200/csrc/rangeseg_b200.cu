@@ -44,6 +44,7 @@ constexpr size_t kSmemLimit = 227 * 1024 - 4096;
 // static shared memory of each CTA
 constexpr size_t kFastSmemTarget = std::min<size_t>(228 * 1024 / rs::kFastOcc - 1024 - 2560, kSmemLimit);
 constexpr int kMinNodeCap = 512;
+constexpr long long kFillCtas = 148;          // one CTA per SM: below this a batch gets thinner bands
 #ifndef RS_UDYN_MIN_C
 #define RS_UDYN_MIN_C 2   // clusters of at least this many bands grab edges dynamically in the local unions
 #endif
@@ -184,7 +185,7 @@ int pick_dense_rows(const rs_config *cfg) {
     return std::min(R, H);
 }
 
-int make_plan_uncached(const rs_config *cfg, Plan *pl) {
+int make_plan_uncached(const rs_config *cfg, Plan *pl, int32_t batch) {
     int st = validate(cfg);
     if (st) return st;
     const int H = cfg->height, W = cfg->width, n_off = cfg->n_offsets;
@@ -227,6 +228,14 @@ int make_plan_uncached(const rs_config *cfg, Plan *pl) {
     int Rf = cfg->rows_per_cta > 0 ? std::min(cfg->rows_per_cta, H)
                                    : std::min({H, kMaxRowsFast, std::max(1, 65536 / std::max(W, 1))});
     while (cfg->rows_per_cta <= 0 && (H + Rf - 1) / Rf > kMaxCluster && Rf < kMaxRowsFast) ++Rf;
+    // Small batches (the reference's one frame per call): a batch that fills
+    // fewer than kFillCtas CTA slots is latency-bound on one or two SMs per
+    // frame, so its frames are split into more, thinner bands (up to a
+    // 16-CTA cluster per frame).
+    if (cfg->rows_per_cta <= 0 && batch > 0)
+        while (Rf > 1 && (long long)batch * ((H + Rf - 1) / Rf) < kFillCtas &&
+               (H + (Rf + 1) / 2 - 1) / ((Rf + 1) / 2) <= kMaxCluster)
+            Rf = (Rf + 1) / 2;
     for (; Rf >= 1; Rf = cfg->rows_per_cta > 0 ? 0 : Rf / 2) {
         if ((H + Rf - 1) / Rf > kMaxCluster) break;
         const int cap_full = max_runs(Rf, W);
@@ -263,6 +272,7 @@ int make_plan_uncached(const rs_config *cfg, Plan *pl) {
 // time, and planning (a capacity search per band height) costs microseconds.
 struct PlanCache {
     bool valid = false;
+    int32_t batch = 0;
     rs_config cfg;
     Plan pl;
     int st = RS_OK;
@@ -270,15 +280,18 @@ struct PlanCache {
 };
 thread_local PlanCache g_plan_cache;
 
-int make_plan(const rs_config *cfg, Plan *pl) {
+// batch 0: the plan of a large batch (what rs_plan reports)
+int make_plan(const rs_config *cfg, Plan *pl, int32_t batch = 0) {
     if (!cfg) return fail(RS_EINVAL, "config is NULL");
     PlanCache &c = g_plan_cache;
-    if (c.valid && memcmp(&c.cfg, cfg, sizeof(rs_config)) == 0) {
+    if (batch >= kFillCtas) batch = 0;   // every large batch has the same plan
+    if (c.valid && c.batch == batch && memcmp(&c.cfg, cfg, sizeof(rs_config)) == 0) {
         if (c.st) return fail(c.st, c.err);
         *pl = c.pl;
         return RS_OK;
     }
-    const int st = make_plan_uncached(cfg, pl);
+    const int st = make_plan_uncached(cfg, pl, batch);
+    c.batch = batch;
     c.cfg = *cfg;
     c.st = st;
     c.err = st ? g_err : std::string();
@@ -402,9 +415,11 @@ int rs_plan(const rs_config *cfg, int32_t *rows_per_cta, int32_t *ctas_per_frame
     return RS_OK;
 }
 
-int rs_plan_detail(const rs_config *cfg, int32_t *out, int32_t n) {
+int rs_plan_detail(const rs_config *cfg, int32_t *out, int32_t n) { return rs_plan_batch(cfg, 0, out, n); }
+
+int rs_plan_batch(const rs_config *cfg, int32_t batch, int32_t *out, int32_t n) {
     Plan pl;
-    int st = make_plan(cfg, &pl);
+    int st = make_plan(cfg, &pl, std::max(batch, 0));
     if (st) return st;
     const int32_t v[] = {pl.fast ? 1 : 0, pl.may_overflow ? 1 : 0, pl.kf.R, pl.kf.C, (int32_t)pl.smem_f, pl.kf.NC,
                          pl.kd.R, pl.kd.C, (int32_t)pl.smem_d};
@@ -416,7 +431,7 @@ int rs_segment_batch(const rs_config *cfg, const float *d_tables, const float *d
                      int32_t *d_labels, int32_t *d_n_clusters, int64_t *d_cluster_sizes, int64_t sizes_stride,
                      void *stream) {
     Plan pl;
-    int st = make_plan(cfg, &pl);
+    int st = make_plan(cfg, &pl, std::max(batch, 0));
     if (st) return st;
     if ((st = validate_outputs(cfg, batch, d_labels, d_cluster_sizes, sizes_stride))) return st;
     if (batch == 0) return RS_OK;
@@ -430,7 +445,7 @@ int rs_segment_batch(const rs_config *cfg, const float *d_tables, const float *d
 int rs_fast_planes(const rs_config *cfg, const float *d_tables, const float *d_ranges, int32_t batch,
                    uint32_t *d_planes, int32_t *d_labels, int32_t *d_n_clusters, void *stream) {
     Plan pl;
-    int st = make_plan(cfg, &pl);
+    int st = make_plan(cfg, &pl, std::max(batch, 0));
     if (st) return st;
     if ((st = validate_outputs(cfg, batch, d_labels, nullptr, 0))) return st;
     if (!pl.fast) return fail(RS_EINVAL, "the fast kernel does not run this geometry (no planes to export)");
@@ -552,7 +567,7 @@ int rs_segment_batch_host(const rs_config *cfg, const float *h_tables, const flo
                           int32_t *h_labels, int32_t *h_n_clusters, int64_t *h_cluster_sizes,
                           int64_t sizes_stride) {
     Plan pl;
-    int st = make_plan(cfg, &pl);
+    int st = make_plan(cfg, &pl, std::max(batch, 0));
     if (st) return st;
     if ((st = validate_outputs(cfg, batch, h_labels, h_cluster_sizes, sizes_stride))) return st;
     if (batch == 0) return RS_OK;

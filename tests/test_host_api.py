@@ -248,3 +248,16 @@ def test_plan_cache_keeps_errors_per_config():
         assert _native.plan(good)[1] >= 1
         with pytest.raises(ValueError, match="rows_per_cta"):
             _native.plan(bad)
+
+
+def test_small_batches_get_thinner_bands():
+    m = rs.fov_model(64, 2.0, -24.8, 2048, 1.73)
+    cfg = _native.make_config(rs.pack_tables(m, rs.PipelineConfig()))
+    big = _native.plan_batch(cfg, 256)
+    assert (big["fast_rows"], big["fast_ctas"]) == (32, 2) == (_native.plan_detail(cfg)["fast_rows"], 2)
+    one = _native.plan_batch(cfg, 1)
+    assert one["fast"] and one["fast_ctas"] == 16 and one["fast_rows"] == 4
+    assert _native.plan_batch(cfg, 40)["fast_ctas"] == 4
+    # an explicit band height is kept
+    cfg.rows_per_cta = 32
+    assert _native.plan_batch(cfg, 1)["fast_rows"] == 32
