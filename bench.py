@@ -403,6 +403,33 @@ def parity_check(pipe, frames):
     return out
 
 
+def time_kernel_graph(pipe, frames, labels, ncl, sizes, steps):
+    """Device time of one launch for a batch too small to keep the GPU busy
+    from Python: the launch is captured in a CUDA graph and the graph is
+    replayed `steps` times between two events (inputs L2-resident: a single
+    frame is 0.5 MB)."""
+    import torch
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        for _ in range(3):
+            pipe.segment_batch(frames, labels=labels, n_clusters=ncl, cluster_sizes=sizes)
+    torch.cuda.current_stream().wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        pipe.segment_batch(frames, labels=labels, n_clusters=ncl, cluster_sizes=sizes)
+    for _ in range(3):
+        g.replay()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    a.record()
+    for _ in range(steps):
+        g.replay()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / steps
+
+
 def time_kernel(pipe, frames, labels, ncl, sizes, steps, flush, stream):
     import torch
     for _ in range(3):
@@ -448,7 +475,9 @@ def per_config_block(args, dev, flush, peak):
         labels = torch.empty((B, spec.H, spec.W), dtype=torch.int32, device=dev)
         ncl = torch.empty((B,), dtype=torch.int32, device=dev)
         sizes = torch.empty((B, pipe.sizes_stride), dtype=torch.int64, device=dev)
-        ms = time_kernel(pipe, frames, labels, ncl, sizes, 30, flush, stream)
+        small = B * spec.H * spec.W * 4 < (64 << 20)   # a single frame: launch-bound from Python
+        ms = (time_kernel_graph(pipe, frames, labels, ncl, sizes, 200) if small
+              else time_kernel(pipe, frames, labels, ncl, sizes, 30, flush, stream))
         cells = B * spec.H * spec.W
         bpc = ALGO_BYTES_PER_CELL + MC_BYTES_PER_OFFSET * len(cfg.mc_pattern)
         e = {"frames": B, "H": spec.H, "W": spec.W, "offsets": len(cfg.mc_pattern),
@@ -456,7 +485,9 @@ def per_config_block(args, dev, flush, peak):
              "ms": ms, "frames_per_s": B / (ms * 1e-3), "points_per_s": cells / (ms * 1e-3),
              "bytes_per_cell": bpc, "frac": cells * bpc / (ms * 1e-3) / 1e9 / peak,
              "compulsory_frac": cells * COMPULSORY_BYTES_PER_CELL / (ms * 1e-3) / 1e9 / peak,
-             "plan": _plan_of(pipe, B)}
+             "plan": _plan_of(pipe, B),
+             "timing": ("CUDA graph replay of the launch, inputs L2-resident (0.5 MB)" if small
+                        else "CUDA events per launch, L2 flushed between launches")}
         if not args.no_check:
             e.update(parity_check(pipe, frames))
         out[label] = e
@@ -487,6 +518,30 @@ def per_frame_api(args, dev, n=300):
             "frames_per_s": 1e3 / float(t.mean()),
             "path": "Pipeline.segment_range_image(numpy [64, 2048] float32) -> LabelImage; pinned staging, "
                     "rs_segment_batch, one sync; config-0 geometry, reference defaults"}
+
+
+def eval_path(frames, model):
+    """SURVEY.md §8(f)3 on the bench frames: the instance-scoring contingency
+    table (rs_contingency, hand-written hash counting) of two segmentations of
+    the batch (gt = default labels, pred = core-variant labels), device-timed,
+    plus the host matching rules (evaluation.match_instances_batch)."""
+    import paper_2003_00575_b200 as rs
+    from paper_2003_00575_b200 import evaluation as ev
+    import torch
+    gt = rs.Pipeline(model, rs.PipelineConfig(), device=frames.device).segment_batch(frames).labels.flatten()
+    pred = rs.Pipeline(model, rs.PipelineConfig(ground_removal=False, min_cluster_points=1),
+                       device=frames.device).segment_batch(frames).labels.flatten()
+    B, n = frames.shape[0], frames[0].numel()
+    off = torch.arange(B + 1, dtype=torch.int64, device=frames.device) * n
+    ms = ev.contingency_device_ms(gt, pred, off)
+    t0 = time.perf_counter()
+    out = ev.match_instances_batch(gt, pred, off, ev.EvalConfig(min_gt_points=100))
+    match_ms = (time.perf_counter() - t0) * 1e3
+    return {"frames": B, "points": B * n, "contingency_device_ms": ms,
+            "points_per_s": B * n / (ms * 1e-3), "input_bytes": 8 * B * n,
+            "hbm_frac": 8 * B * n / (ms * 1e-3) / 1e9 / measured_peak()[0],
+            "match_host_ms": match_ms, "instances_scored": sum(len(o) for o in out),
+            "path": "rs_contingency (per-frame shared-memory hash + sort) -> host matching rules"}
 
 
 def run_b200(args):
@@ -582,9 +637,10 @@ def run_b200(args):
             dist.destroy_process_group()
         return
 
-    cloud_path = None
+    cloud_path = eval_p = None
     if not args.no_cloud and world == 1:
         cloud_path = cloud_bench(args, pipe, frames, spec, flush)
+        eval_p = eval_path(frames, model)
 
     cpu = cpu_port = None
     if not args.no_cpu_baseline:
@@ -646,6 +702,7 @@ def run_b200(args):
         "per_frame_api": frame_api,
         "per_config": per_config,
         "cloud_path": cloud_path,
+        "eval_path": eval_p,
         "gpu_launches": args.steps,   # one rs_fast_kernel (or rs_dense_kernel) launch per step
         "clocks": clk.summary(),
         "wall_s_timed_region": wall,

@@ -194,13 +194,15 @@ int rs_labels_to_points(const int32_t *d_labels, const int64_t *d_point_index, c
  * frames, the counting step of evaluation.match_instances.  gt / pred: int32
  * per point (0 = none / background, values < 2^22), frames concatenated with
  * int64 CSR offsets [B+1] (B < 2^19), all device.  Output: d_pairs /
- * d_counts (int64, capacity n_points) hold the sorted unique keys
+ * d_counts (int64, capacity n_points + 1) hold the sorted unique keys
  * (frame << 44 | gt << 22 | pred) over points with gt > 0 or pred > 0 and their
  * point counts; a last key 0x7fffffffffffffff (if present) counts the points
  * with gt == pred == 0 and is not a pair.  d_status int64 [2] = (number of
  * keys, 1 if a label was out of range).  Sizes of instances and clusters are
- * the row / column sums.  Asynchronous on `stream`. */
-size_t rs_contingency_workspace_size(int64_t n_points);
+ * the row / column sums.  Counted per frame in a shared-memory hash table
+ * (hand-written kernels, rs_eval.cuh); no initialisation of the workspace is
+ * needed.  Asynchronous on `stream`. */
+size_t rs_contingency_workspace_size(int64_t n_points, int32_t n_frames);
 int rs_contingency(const int32_t *d_gt, const int32_t *d_pred, const int64_t *d_offsets, int32_t n_frames,
                    int64_t n_points, int64_t *d_pairs, int64_t *d_counts, int64_t *d_status,
                    void *d_workspace, size_t workspace_size, void *stream);

@@ -89,7 +89,7 @@ def lib():
         L.rs_labels_to_points.argtypes = [_P, _P, _P, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
                                           ctypes.c_int64, _P, _P]
         L.rs_contingency_workspace_size.restype = ctypes.c_size_t
-        L.rs_contingency_workspace_size.argtypes = [ctypes.c_int64]
+        L.rs_contingency_workspace_size.argtypes = [ctypes.c_int64, ctypes.c_int32]
         L.rs_contingency.restype = ctypes.c_int
         L.rs_contingency.argtypes = [_P, _P, _P, ctypes.c_int32, ctypes.c_int64, _P, _P, _P, _P,
                                      ctypes.c_size_t, _P]

@@ -26,8 +26,6 @@
 #include "rs_project.cuh"
 #include "rs_eval.cuh"
 
-#include <cub/device/device_radix_sort.cuh>
-#include <cub/device/device_run_length_encode.cuh>
 
 using rs::KArgs;
 
@@ -731,23 +729,30 @@ int rs_labels_to_points(const int32_t *d_labels, const int64_t *d_point_index, c
     return cuda_check(cudaGetLastError(), "rs_labels_to_points launch");
 }
 
-// workspace of rs_contingency: keys in, keys sorted, the invalid-label flag,
-// then CUB's temporary storage (256-byte aligned pieces)
+// workspace of rs_contingency: per frame count / offset / none count (u64
+// each), the invalid-label flag, then the per-frame scratch (rs_eval.cuh):
+// 4 (n_points + B) keys (u64) and counts (u32).  B is bounded by n_points + 1
+// for the size query (frames may be empty), so it is taken from the caller.
 namespace {
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
-size_t cub_temp_bytes(int n) {
-    size_t a = 0, b = 0;
-    cub::DeviceRadixSort::SortKeys(nullptr, a, (const long long *)nullptr, (long long *)nullptr, n);
-    cub::DeviceRunLengthEncode::Encode(nullptr, b, (const long long *)nullptr, (long long *)nullptr,
-                                       (long long *)nullptr, (long long *)nullptr, n);
-    return std::max(a, b);
+struct ContLayout {
+    size_t frames, flag, keys, cnts, total;
+};
+ContLayout cont_layout(int64_t n_points, int64_t n_frames) {
+    ContLayout l;
+    const size_t ent = 4 * ((size_t)std::max<int64_t>(n_points, 0) + (size_t)std::max<int64_t>(n_frames, 0));
+    l.frames = 0;
+    l.flag = align256(3 * 8 * (size_t)std::max<int64_t>(n_frames, 1));
+    l.keys = l.flag + 256;
+    l.cnts = l.keys + align256(ent * 8);
+    l.total = l.cnts + align256(ent * 4);
+    return l;
 }
 }  // namespace
 
-size_t rs_contingency_workspace_size(int64_t n_points) {
-    if (n_points < 0 || n_points >= (1LL << 31)) return 0;
-    const int n = (int)n_points;
-    return 2 * align256((size_t)n * 8) + 256 + align256(cub_temp_bytes(std::max(n, 1)));
+size_t rs_contingency_workspace_size(int64_t n_points, int32_t n_frames) {
+    if (n_points < 0 || n_points >= (1LL << 31) || n_frames < 0) return 0;
+    return cont_layout(n_points, n_frames).total;
 }
 
 int rs_contingency(const int32_t *d_gt, const int32_t *d_pred, const int64_t *d_offsets, int32_t n_frames,
@@ -756,35 +761,36 @@ int rs_contingency(const int32_t *d_gt, const int32_t *d_pred, const int64_t *d_
     if (n_frames < 0 || n_points < 0) return fail(RS_EINVAL, "negative sizes");
     if (n_frames >= (1 << rs::kEvalFrameBits)) return fail(RS_ETOOLARGE, "at most 2^19 - 1 frames per call");
     if (n_points >= (1LL << 31)) return fail(RS_ETOOLARGE, "at most 2^31 - 1 points per call");
-    if (workspace_size < rs_contingency_workspace_size(n_points))
-        return fail(RS_EINVAL, "workspace smaller than rs_contingency_workspace_size(n_points)");
+    if (workspace_size < rs_contingency_workspace_size(n_points, n_frames))
+        return fail(RS_EINVAL, "workspace smaller than rs_contingency_workspace_size(n_points, n_frames)");
     if (!d_status || (n_points > 0 && (!d_gt || !d_pred || !d_offsets || !d_pairs || !d_counts || !d_workspace)))
         return fail(RS_EINVAL, "NULL buffer");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     int st;
     if ((st = cuda_check(cudaMemsetAsync(d_status, 0, 2 * sizeof(int64_t), s), "memset status"))) return st;
     if (n_points == 0 || n_frames == 0) return RS_OK;
-    const int n = (int)n_points;
+    const ContLayout l = cont_layout(n_points, n_frames);
     char *w = static_cast<char *>(d_workspace);
-    long long *keys = reinterpret_cast<long long *>(w);
-    long long *sorted = reinterpret_cast<long long *>(w + align256((size_t)n * 8));
-    int *bad = reinterpret_cast<int *>(w + 2 * align256((size_t)n * 8));
-    void *temp = w + 2 * align256((size_t)n * 8) + 256;
-    size_t temp_bytes = cub_temp_bytes(n);
+    auto *frame_n = reinterpret_cast<unsigned long long *>(w);
+    auto *frame_off = frame_n + n_frames;
+    auto *frame_none = frame_off + n_frames;
+    int *bad = reinterpret_cast<int *>(w + l.flag);
+    auto *K = reinterpret_cast<unsigned long long *>(w + l.keys);
+    auto *C = reinterpret_cast<uint32_t *>(w + l.cnts);
+    static bool attr_set = false;   // per process; the attribute is per function, any device of one arch
+    if (!attr_set) {
+        if ((st = cuda_check(cudaFuncSetAttribute(rs::rs_cont_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                  (int)rs::kEvalSmem), "cudaFuncSetAttribute(contingency)")))
+            return st;
+        attr_set = true;
+    }
     if ((st = cuda_check(cudaMemsetAsync(bad, 0, sizeof(int), s), "memset flag"))) return st;
-    rs::rs_contingency_keys_kernel<<<(unsigned)((n + rs::kEvalThreads - 1) / rs::kEvalThreads), rs::kEvalThreads, 0,
-                                     s>>>(d_gt, d_pred, d_offsets, n_frames, n_points, keys, bad);
-    if ((st = cuda_check(cudaGetLastError(), "contingency keys")) ||
-        (st = cuda_check(cub::DeviceRadixSort::SortKeys(temp, temp_bytes, keys, sorted, n, 0, 64, s),
-                         "radix sort")) ||
-        (st = cuda_check(cub::DeviceRunLengthEncode::Encode(temp, temp_bytes, sorted,
-                                                            reinterpret_cast<long long *>(d_pairs),
-                                                            reinterpret_cast<long long *>(d_counts),
-                                                            reinterpret_cast<long long *>(d_status), n, s),
-                         "run-length encode")) ||
-        (st = cuda_check(cudaMemcpyAsync(d_status + 1, bad, sizeof(int), cudaMemcpyDeviceToDevice, s), "flag")))
-        return st;
-    return RS_OK;
+    rs::rs_cont_count_kernel<<<n_frames, rs::kEvalThreads, rs::kEvalSmem, s>>>(d_gt, d_pred, d_offsets, K, C, frame_n,
+                                                                              frame_none, bad);
+    rs::rs_cont_scan_kernel<<<1, 1024, 0, s>>>(n_frames, frame_n, frame_none, frame_off, d_pairs, d_counts, d_status,
+                                              bad);
+    rs::rs_cont_move_kernel<<<n_frames, 256, 0, s>>>(d_offsets, K, C, frame_n, frame_off, d_pairs, d_counts);
+    return cuda_check(cudaGetLastError(), "rs_contingency launch");
 }
 
 int rs_phase_profile(int64_t *host_out, int32_t max_ctas) {

@@ -91,10 +91,10 @@ def contingency_batch(gt: torch.Tensor, pred: torch.Tensor, offsets: torch.Tenso
     n = gt.numel()
     B = offsets.numel() - 1
     dev = gt.device
-    pairs = torch.empty((max(n, 1),), dtype=torch.int64, device=dev)
-    counts = torch.empty((max(n, 1),), dtype=torch.int64, device=dev)
+    pairs = torch.empty((n + 1,), dtype=torch.int64, device=dev)
+    counts = torch.empty((n + 1,), dtype=torch.int64, device=dev)
     status = torch.empty((2,), dtype=torch.int64, device=dev)
-    wsb = int(_native.lib().rs_contingency_workspace_size(n))
+    wsb = int(_native.lib().rs_contingency_workspace_size(n, B))
     ws = torch.empty((max(wsb, 8),), dtype=torch.uint8, device=dev)
     s = stream if stream is not None else torch.cuda.current_stream(dev)
     st = _native.lib().rs_contingency(_ptr(gt.contiguous()), _ptr(pred.contiguous()), _ptr(offsets), B, n,
@@ -110,6 +110,33 @@ def contingency_batch(gt: torch.Tensor, pred: torch.Tensor, offsets: torch.Tenso
     keys, cnt = keys[keep], cnt[keep]
     mask = (1 << _LABEL_BITS) - 1
     return keys >> (2 * _LABEL_BITS), (keys >> _LABEL_BITS) & mask, keys & mask, cnt
+
+
+def contingency_device_ms(gt: torch.Tensor, pred: torch.Tensor, offsets: torch.Tensor, reps: int = 10) -> float:
+    """Device time (CUDA events) of one rs_contingency call on these labels."""
+    n = gt.numel()
+    B = offsets.numel() - 1
+    dev = gt.device
+    pairs = torch.empty((n + 1,), dtype=torch.int64, device=dev)
+    counts = torch.empty((n + 1,), dtype=torch.int64, device=dev)
+    status = torch.empty((2,), dtype=torch.int64, device=dev)
+    wsb = int(_native.lib().rs_contingency_workspace_size(n, B))
+    ws = torch.empty((max(wsb, 8),), dtype=torch.uint8, device=dev)
+    s = torch.cuda.current_stream(dev)
+
+    def call():
+        _native.check(_native.lib().rs_contingency(_ptr(gt), _ptr(pred), _ptr(offsets), B, n, _ptr(pairs),
+                                                   _ptr(counts), _ptr(status), _ptr(ws), wsb,
+                                                   ctypes.c_void_p(s.cuda_stream)), "rs_contingency")
+    for _ in range(3):
+        call()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        call()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / reps
 
 
 def _match_table(g_ids, c_ids, cnt, cfg: EvalConfig):
