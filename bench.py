@@ -57,6 +57,7 @@ def parse():
     p.add_argument("--no-cloud", action="store_true", help="skip the point-cloud path measurement")
     p.add_argument("--no-per-config", action="store_true", help="skip the per-config block")
     p.add_argument("--no-check", action="store_true", help="skip the parity checks against the oracle")
+    p.add_argument("--no-frame-api", action="store_true", help="skip the per-frame API latency")
     return p.parse_args()
 
 
@@ -664,7 +665,7 @@ def run_b200(args):
     per_config = None
     if not args.no_per_config and world == 1:
         per_config = per_config_block(args, dev, flush, peak)
-    frame_api = per_frame_api(args, dev) if world == 1 else None
+    frame_api = per_frame_api(args, dev) if world == 1 and not args.no_frame_api else None
     check = None
     if not args.no_check:
         check = parity_check(pipe, frames)

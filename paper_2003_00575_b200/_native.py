@@ -45,8 +45,35 @@ class RsProjectConfig(ctypes.Structure):
 
 
 _lib = None
+_ext = None
 
 _P = ctypes.c_void_p
+EXT_PATH = LIB_PATH.parent / "torch_ext" / "rangeseg_b200_torch.so"
+
+
+def use_torch_ext() -> bool:
+    """The PyTorch extension links the in-tree librangeseg_b200.so; an RS_LIB
+    override (experiment variants, scripts/ab.sh) goes through ctypes only."""
+    return not os.environ.get("RS_LIB")
+
+
+def torch_ext():
+    """The thin PyTorch C++ extension over the C ABI (csrc/torch_ext.cpp):
+    tensors in, rs_segment_batch on the current stream with the GIL released.
+    Built in-tree by ``build.build_torch_ext`` (no JIT build at import)."""
+    global _ext
+    if _ext is None:
+        import importlib.util
+
+        import torch  # noqa: F401  (libc10 / libtorch for the extension)
+        lib()          # the C library the extension links (and its error if missing)
+        if not EXT_PATH.exists():
+            raise RuntimeError(f"PyTorch extension {EXT_PATH} is missing; run __graft_entry__.build()")
+        spec = importlib.util.spec_from_file_location("rangeseg_b200_torch", str(EXT_PATH))
+        mod = importlib.util.module_from_spec(spec)
+        spec.loader.exec_module(mod)
+        _ext = mod
+    return _ext
 
 
 def lib():

@@ -58,6 +58,28 @@ def build(force: bool = False, verbose: bool = False, profile: bool = False,
     return out
 
 
+TORCH_EXT_DIR = PKG / "_lib" / "torch_ext"
+TORCH_EXT_NAME = "rangeseg_b200_torch"
+TORCH_EXT_SRC = PKG / "csrc" / "torch_ext.cpp"
+
+
+def build_torch_ext(force: bool = False) -> Path:
+    """The thin PyTorch C++ extension over the C ABI (csrc/torch_ext.cpp),
+    built in-tree next to librangeseg_b200.so (rpath $ORIGIN/..)."""
+    out = TORCH_EXT_DIR / f"{TORCH_EXT_NAME}.so"
+    deps = [TORCH_EXT_SRC, INCLUDE / "rangeseg_b200.h", OUT]
+    if not force and out.exists() and all(out.stat().st_mtime >= d.stat().st_mtime for d in deps):
+        return out
+    from torch.utils import cpp_extension
+    TORCH_EXT_DIR.mkdir(parents=True, exist_ok=True)
+    cpp_extension.load(name=TORCH_EXT_NAME, sources=[str(TORCH_EXT_SRC)], build_directory=str(TORCH_EXT_DIR),
+                       extra_include_paths=[str(INCLUDE)], extra_cflags=["-O2", "-std=c++17"],
+                       extra_ldflags=[f"-L{OUT.parent}", "-lrangeseg_b200", "-Wl,-rpath,\\$$ORIGIN/.."],
+                       with_cuda=True, verbose=False)
+    out.touch()
+    return out
+
+
 if __name__ == "__main__":
     import sys
     print(build(force=True, verbose=True, profile="--profile" in sys.argv))

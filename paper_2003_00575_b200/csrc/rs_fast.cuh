@@ -196,12 +196,16 @@ struct BitsStrip {
     int ch, lane, r0, rstart, rend, cb;
     float thr, tch;
     int rfirst;   // first row walked (rstart, or a later row when rows are split between warps)
-    int rowb;     // bytes per row (4 W)
+    int rowf;     // floats per row (W)
     int wpb;      // bytes per plane row (4 WPR)
     mutable uint32_t mx = 0;   // unsigned max of the raw bits of the rows walked (input-contract screen)
 
+    mutable const float *np = nullptr;   // the row the next step prefetches (advanced by a row per step)
+
     __device__ __forceinline__ void ld4(int r, float (&x)[4], bool pred = true) const {
-        const float *p = col + (size_t)r * a.W;
+        ldp(col + r * rowf, x, pred);   // 32-bit offset: a frame has < 2^24 cells
+    }
+    __device__ __forceinline__ void ldp(const float *p, float (&x)[4], bool pred = true) const {
 #pragma unroll
         for (int j = 0; j < 4; ++j)
             if (pred && (FULL || cb + 32 * j < a.W)) {
@@ -219,7 +223,10 @@ struct BitsStrip {
     template <bool ROW0, bool HALO = false>
     __device__ __forceinline__ void step(int r, const float (&va)[4], const float (&v)[4], const float (&vb)[4],
                                          float (&vn)[4]) const {
-        if (!ROW0) ld4(r + RS_STRIP_SETS - 2, vn, r + RS_STRIP_SETS - 2 < rend);
+        if (!ROW0) {   // prefetch row r + RS_STRIP_SETS - 2
+            ldp(np, vn, r + RS_STRIP_SETS - 2 < rend);
+            np += rowf;
+        }
         const float4 c = *reinterpret_cast<const float4 *>(rowc + (r - rstart) * 8);
         const float4 c2 = *reinterpret_cast<const float4 *>(rowc + (r - rstart) * 8 + 4);
         const int srcl = (lane + 31) & 31;
@@ -280,6 +287,7 @@ struct BitsStrip {
         if (rf >= rend) return;
         ld4(rf - 1, S0);
         ld4(rf, S1);
+        np = col + (rf + 1) * rowf;
         if (rf < r0) {
             // the halo row (first row walked in a band > 0): P / L only
             step<false, true>(rf, S0, S1, S1, S2);
@@ -320,6 +328,7 @@ struct BitsStrip {
         ld4(rf - 1, S0);
         ld4(rf, S1);
         ld4(rf + 1, S2, rf + 1 < rend);
+        np = col + (rf + 2) * rowf;
         if (rf < r0) {
             // the halo row (first row walked in a band > 0): P / L only
             step<false, true>(rf, S0, S1, S2, S3);
@@ -415,7 +424,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
 #define RS_STRIP(F, G)                                                                                          \
     do {                                                                                                    \
         const BitsStrip<F, G> st{a, fr + cb, rowc, sP, sL, sU, sPh, sLh, ch, lane, r0, rstart, rhi, cb, thr, \
-                                      tch, rlo, 4 * W, 4 * WPR};                                            \
+                                      tch, rlo, W, 4 * WPR};                                            \
         st.run();                                                                                           \
         umx = max(umx, st.mx);                                                                              \
     } while (0)

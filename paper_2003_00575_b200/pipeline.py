@@ -154,6 +154,7 @@ class Pipeline:
         self._tables = None
         self._tables_host = np.ascontiguousarray(self.packed.block, dtype=np.float32)
         self._frame_bufs = None   # pinned staging of segment_range_image
+        self._no_sizes = torch.empty(0, dtype=torch.int64)
 
     # -- helpers -----------------------------------------------------------
     @property
@@ -244,11 +245,17 @@ class Pipeline:
                 for t in (ranges, labels, n_clusters, cluster_sizes, self.device_tables()):
                     if t is not None:
                         t.record_stream(s)
-            st = _native.lib().rs_segment_batch(
-                ctypes.byref(self.rs_config), _ptr(self.device_tables()), _ptr(ranges), B,
-                _ptr(labels), _ptr(n_clusters), _ptr(cluster_sizes), stride,
-                ctypes.c_void_p(s.cuda_stream))
-        _native.check(st, "rs_segment_batch")
+            if _native.use_torch_ext():
+                # the thin PyTorch extension over rs_segment_batch (GIL released, current stream)
+                with torch.cuda.stream(s):
+                    _native.torch_ext().segment_batch(
+                        ctypes.addressof(self.rs_config), self.device_tables(), ranges, labels, n_clusters,
+                        cluster_sizes if cluster_sizes is not None else self._no_sizes)
+            else:
+                _native.check(_native.lib().rs_segment_batch(
+                    ctypes.byref(self.rs_config), _ptr(self.device_tables()), _ptr(ranges), B,
+                    _ptr(labels), _ptr(n_clusters), _ptr(cluster_sizes), stride,
+                    ctypes.c_void_p(s.cuda_stream)), "rs_segment_batch")
         return BatchResult(labels, n_clusters, cluster_sizes)
 
     def fast_planes(self, ranges: torch.Tensor):

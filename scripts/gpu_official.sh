@@ -9,7 +9,7 @@ timeout 900 python bench.py > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TA
 tail -c 600 gpurun_out/bench_$TAG.json
 timeout 900 python bench.py --impl reference --steps 20 --warmup 2 > gpurun_out/bench_ref_$TAG.json 2>&1; echo ref rc=$?
 tail -c 400 gpurun_out/bench_ref_$TAG.json
-Q="--steps 5 --warmup 3 --no-cpu-baseline --no-e2e --no-cloud --no-per-config --no-check"
+Q="--steps 5 --warmup 3 --no-cpu-baseline --no-e2e --no-cloud --no-per-config --no-check --no-frame-api"
 python bench.py $Q > gpurun_out/plain_launch_$TAG.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:rs_ -c 40 --csv --log-file gpurun_out/launches_$TAG.csv python bench.py $Q > gpurun_out/ncu_launch_$TAG.log 2>&1
 echo launches rc=$?

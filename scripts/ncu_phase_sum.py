@@ -19,8 +19,8 @@ tot = [0, 0]
 for t in tables:
     for r in t:
         tot[0] += int(r[iS] or 0); tot[1] += int(r[iI] or 0)
-# rs_fast.cuh is the table that holds the run_of helper
-fast = next(t for t in tables if any("__popc(SB[w] & lanemask_le(b))" in r[1] for r in t))
+# rs_fast.cuh is the table that holds struct BitsStrip
+fast = next(t for t in tables if any("pw[j] = __ballot_sync" in r[1] for r in t))
 print(f"total samples {tot[0]} warp-instr {tot[1]}")
 for name, lo, hi in ranges:
     s = sum(int(r[iS] or 0) for r in fast if lo <= int(r[0]) <= hi)

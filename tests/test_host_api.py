@@ -261,3 +261,10 @@ def test_small_batches_get_thinner_bands():
     # an explicit band height is kept
     cfg.rows_per_cta = 32
     assert _native.plan_batch(cfg, 1)["fast_rows"] == 32
+
+
+def test_torch_extension_loads_and_matches_abi():
+    """The thin PyTorch extension (csrc/torch_ext.cpp) links the same C ABI."""
+    ext = _native.torch_ext()
+    assert ext.abi_version() == _native.lib().rs_version()
+    assert hasattr(ext, "segment_batch")
