@@ -234,11 +234,6 @@ struct BitsStrip {
         uint32_t pw[4], lw[4], uw[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-#ifndef RS_NO_SCREEN
-            // input-contract screen on the row being decided (every row of the
-            // walk is the current row exactly once; no wait on a prefetch)
-            mx = max(mx, __float_as_uint(v[j]));
-#endif
             const float d1 = ROW0 ? v[j] : va[j];
             const float d2 = ROW0 ? vb[j] : v[j];
             const bool gr = GROUND && ground_fast(c.x, c.y, c.z, c.w, c2.x, c2.z, d1, d2, v[j], ROW0 ? vb[j] : va[j]);
@@ -250,6 +245,13 @@ struct BitsStrip {
             lw[j] = __ballot_sync(kFull, pair_pass(vl, v[j], tch, thr));
             uw[j] = ROW0 ? 0u : __ballot_sync(kFull, pair_pass(va[j], v[j], c2.y, thr));
         }
+#ifndef RS_NO_SCREEN
+        // input-contract screen on the row just decided (every row of the walk
+        // is the current row exactly once; its values are in registers by
+        // now): two 3-input unsigned max (VIMNMX3) for the lane's four cells
+        mx = __vimax3_u32(mx, __float_as_uint(v[0]), __float_as_uint(v[1]));
+        mx = __vimax3_u32(mx, __float_as_uint(v[2]), __float_as_uint(v[3]));
+#endif
         const bool halo = HALO;   // only the first row walked in a band > 0 (peeled in run())
         const int cw = ch * 4;
         const uint32_t off = halo ? 0u : (uint32_t)((r - r0) * wpb);
