@@ -68,6 +68,26 @@ __device__ long long g_prof[kProfCtas * kProfSlots];
     } while (0)
 #endif
 
+// ------------------------------------------------------------ bounds checks
+// RS_CHECKED builds (scripts/gpu_checked.sh) trap on any out-of-range index
+// into shared memory, DSMEM or the outputs — the substitute for
+// compute-sanitizer memcheck, which this GPU pool does not allow.
+#ifdef RS_CHECKED
+#include <cstdio>
+#define RS_CHECK(cond, what)                                                                                 \
+    do {                                                                                                   \
+        if (!(cond)) {                                                                                     \
+            printf("RS_CHECK failed: %s (%s:%d) block %d thread %d\n", what, __FILE__, __LINE__, blockIdx.x, \
+                   threadIdx.x);                                                                           \
+            __trap();                                                                                      \
+        }                                                                                                  \
+    } while (0)
+#else
+#define RS_CHECK(cond, what) \
+    do {                     \
+    } while (0)
+#endif
+
 // ---------------------------------------------------------------- arithmetic
 
 // pair_distance_sq (connectivity.py:54) compared with d_max_sq: five separately
@@ -207,6 +227,7 @@ __device__ __forceinline__ uint32_t lanemask_le(int lane) {
 // Run id of cell bit b of word w (fast kernel): runs started at or before the
 // cell in this word, plus the runs started before the word.
 __device__ __forceinline__ uint32_t run_of(const uint32_t *SB, const uint32_t *NB, int w, int b) {
+    RS_CHECK(w >= 0 && b >= 0 && b < 32, "run_of word/bit");
     return NB[w] + __popc(SB[w] & lanemask_le(b)) - 1u;
 }
 

@@ -78,8 +78,12 @@ struct RunUF {
     int SHN;
     int rank;
 
+    int nc;   // node capacity per band (RS_CHECKED)
+    int C;    // bands in the cluster (RS_CHECKED)
+
     __device__ __forceinline__ uint32_t *slot(uint32_t *arr, uint32_t e) const {
         const int owner = (int)(e >> SHN);
+        RS_CHECK(owner < C && (int)(e & mask) < nc, "union-find node out of range");
         return (owner == rank ? arr : cl.map_shared_rank(arr, owner)) + (e & mask);
     }
     __device__ __forceinline__ uint32_t ld(uint32_t e) const {
@@ -544,6 +548,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
     }
     if (tid == 0) ovf = n_runs > (uint32_t)a.NC;
     const bool overflow = n_runs > (uint32_t)a.NC;   // block-uniform
+    RS_CHECK(overflow || n_runs <= (uint32_t)a.NC, "run count");
     if (!overflow) {
         for (int w = wr0 + lane; w < wr1; w += 32) NB[w] += my_off;
         for (uint32_t id = tid; id < n_runs; id += kFastThreads) {
@@ -555,7 +560,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
     RS_MARK(3);
     RS_STOP(2);
 
-    RunUF uf{E, cl, maskN, a.SHN, k};
+    RunUF uf{E, cl, maskN, a.SHN, k, a.NC, a.C};
     if (!overflow) {
         // ---- U. band-local unions ----------------------------------------------
         // Edges are gathered into a list (the size array is the buffer; it is
@@ -599,6 +604,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
                 }
                 if (!k) continue;
                 auto push = [&](uint32_t x, uint32_t y) {
+                    RS_CHECK(x < n_runs && y < n_runs, "listed edge run ids");
                     if (direct) uf.unite_local(band | x, band | y);
                     else if (slot < cap) EL[slot] = (x << 16) | y;
                     ++slot;
@@ -972,6 +978,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
             uint32_t label = 0;
             if ((km >> b) & 1u) {
                 label = cta_pre[owner] + wk + __popc(km & ((1u << b) - 1u)) + 1u;
+                RS_CHECK(!a.sizes || (int64_t)label < a.sizes_stride, "cluster_sizes row");
                 if (g == (band | id) && a.sizes) a.sizes[(size_t)frame * a.sizes_stride + label] = (int64_t)SZ[id];
             }
             SZ[id] = label;   // only this thread read SZ[id] (the root's size)

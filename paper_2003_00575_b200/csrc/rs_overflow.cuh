@@ -70,6 +70,7 @@ __device__ __forceinline__ int ovf_root(const int *par, int e) {
 }
 
 __device__ __forceinline__ void ovf_unite(int *par, int x, int y) {
+    RS_CHECK(x >= 0 && y >= 0, "overflow union-find cell");
     while (true) {
         x = ovf_find(par, x);
         y = ovf_find(par, y);

@@ -48,41 +48,57 @@ struct ProjArgs {
     unsigned long long *rbits;   // [n_total] workspace: float64 range bits of each point
 };
 
-// Adds `v` (per thread) to counts[2*b + slot], with one global atomic per
-// block when the whole block works on one cloud (the usual case), else per
+// Adds `v` (0 or 1 per thread) to counts[2*b + slot]: one barrier-count and
+// one global atomic per block when the whole block works on one cloud (the
+// usual case; per-warp atomics on one hot counter serialise in L2), else per
 // (warp, cloud).  Every thread of the block must call it.
 __device__ __forceinline__ void count_add(int64_t *counts, int b, int slot, unsigned v) {
     __shared__ int sb_first, sb_last;
-    __shared__ unsigned long long s_sum;
-    if (threadIdx.x == 0) { sb_first = b; s_sum = 0; }
+    if (threadIdx.x == 0) sb_first = b;
     if (threadIdx.x == blockDim.x - 1) sb_last = b;
-    __syncthreads();
-    const bool uniform = sb_first == sb_last && sb_first >= 0;
-    if (uniform) {
-        unsigned w = __reduce_add_sync(0xffffffffu, v);
-        if ((threadIdx.x & 31) == 0 && w) atomicAdd(&s_sum, (unsigned long long)w);
-        __syncthreads();
-        if (threadIdx.x == 0 && s_sum) atomicAdd(reinterpret_cast<unsigned long long *>(counts) + 2 * b + slot, s_sum);
-    } else {
-        const unsigned lanes = __match_any_sync(0xffffffffu, b);
-        unsigned tot = 0;
-        for (unsigned m = lanes; m; m &= m - 1) tot += __shfl_sync(0xffffffffu, v, __ffs(m) - 1);
-        if (b >= 0 && (threadIdx.x & 31) == __ffs(lanes) - 1 && tot)
-            atomicAdd(reinterpret_cast<unsigned long long *>(counts) + 2 * b + slot, (unsigned long long)tot);
+    const int n = __syncthreads_count(v != 0u);   // also orders the two stores above
+    if (sb_first == sb_last && sb_first >= 0) {
+        if (threadIdx.x == 0 && n) atomicAdd(reinterpret_cast<unsigned long long *>(counts) + 2 * b + slot,
+                                             (unsigned long long)n);
+        return;
     }
+    const unsigned lanes = __match_any_sync(0xffffffffu, b);
+    const unsigned tot = __popc(__ballot_sync(0xffffffffu, v != 0u) & lanes);
+    if (b >= 0 && (threadIdx.x & 31) == __ffs(lanes) - 1 && tot)
+        atomicAdd(reinterpret_cast<unsigned long long *>(counts) + 2 * b + slot, (unsigned long long)tot);
 }
 
-__device__ __forceinline__ int cloud_of(const ProjArgs &a, int64_t i) {
-    int lo = 0, hi = a.B;   // offsets[lo] <= i < offsets[hi]
+// cloud of point i (offsets[b] <= i < offsets[b+1]) inside [lo, hi)
+__device__ __forceinline__ int cloud_in(const int64_t *offsets, int64_t i, int lo, int hi) {
     while (hi - lo > 1) {
         const int mid = (lo + hi) >> 1;
-        if (__ldg(a.offsets + mid) <= i) lo = mid; else hi = mid;
+        if (__ldg(offsets + mid) <= i) lo = mid; else hi = mid;
     }
     return lo;
 }
 
-// numpy float64 floor_divide (npy_divmod's quotient) for a >= 0, b > 0
+// Cloud of point i: the block's first and last points are located once (a
+// block nearly always lies inside one cloud), every thread then searches only
+// between them.  Every thread of the block must call it.
+__device__ __forceinline__ int cloud_of_block(const ProjArgs &a, int64_t i) {
+    __shared__ int s_lo, s_hi;
+    const int64_t first = (int64_t)blockIdx.x * blockDim.x;
+    if (threadIdx.x == 0) s_lo = cloud_in(a.offsets, first, 0, a.B);
+    if (threadIdx.x == 32 % blockDim.x)
+        s_hi = cloud_in(a.offsets, (first + blockDim.x < a.n_total ? first + blockDim.x : a.n_total) - 1, 0, a.B) + 1;
+    __syncthreads();
+    return cloud_in(a.offsets, i, s_lo, s_hi);
+}
+
+// numpy float64 floor_divide (npy_divmod's quotient) for a >= 0, b > 0: the
+// integer k with x = k*y + fmod(x, y), i.e. the floor of the exact quotient.
+// Fast path: t = x / y rounded is within an ulp of the exact quotient, so
+// floor(t) is the answer unless t lies within 1e-9 of an integer; only those
+// (a measure-zero set of azimuths at column edges) take numpy's exact steps.
 __device__ __forceinline__ double py_floor_divide(double x, double y) {
+    const double t = __ddiv_rn(x, y);
+    const double ft = floor(t);
+    if (__dsub_rn(t, ft) > 1e-9 && __dsub_rn(__dadd_rn(ft, 1.0), t) > 1e-9 && t < 4.0e6) return ft;
     const double mod = fmod(x, y);
     const double div = __ddiv_rn(__dsub_rn(x, mod), y);
     if (div == 0.0) return copysign(0.0, __ddiv_rn(x, y));
@@ -123,8 +139,9 @@ __global__ void __launch_bounds__(kProjThreads) rs_project_min_kernel(const __gr
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     int b = -1;
     int64_t cell = -1;
+    const int bi = cloud_of_block(a, i);
     if (i < a.n_total) {
-        b = cloud_of(a, i);
+        b = bi;
         double r;
         cell = proj_cell(a, a.pts + i * a.stride, r);
         a.cell[i] = (int32_t)cell;
@@ -138,10 +155,11 @@ __global__ void __launch_bounds__(kProjThreads) rs_project_min_kernel(const __gr
 
 __global__ void __launch_bounds__(kProjThreads) rs_project_index_kernel(const __grid_constant__ ProjArgs a) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int bi = cloud_of_block(a, i);
     if (i >= a.n_total) return;
     const int32_t cell = a.cell[i];
     if (cell < 0) return;
-    const int b = cloud_of(a, i);
+    const int b = bi;
     const int64_t q = (int64_t)b * a.H * a.W + cell;
     const unsigned long long m = reinterpret_cast<const unsigned long long *>(a.point_index)[q];
     if (m == a.rbits[i])

@@ -141,7 +141,8 @@ class Pipeline:
     """
 
     def __init__(self, model: SensorModel, config: PipelineConfig | None = None,
-                 device=None, rows_per_cta: int = 0, node_capacity: int = 0):
+                 device=None, rows_per_cta: int = 0, node_capacity: int = 0,
+                 stage_timing: bool = False):
         self.model = model
         self.config = config or PipelineConfig()
         self.packed = pack_tables(model, self.config)
@@ -154,6 +155,11 @@ class Pipeline:
         self._tables = None
         self._tables_host = np.ascontiguousarray(self.packed.block, dtype=np.float32)
         self._frame_bufs = None   # pinned staging of segment_range_image
+        # per-stage TimingRecord (pipeline.py:94-130): the fused kernel runs every
+        # stage in one launch, so with stage_timing the reference's separate
+        # stages are also run (rs_height_image + rs_ground_mask, rs_connectivity)
+        # and timed on the device; off by default (extra launches)
+        self.stage_timing = bool(stage_timing)
         self._no_sizes = torch.empty(0, dtype=torch.int64)
 
     # -- helpers -----------------------------------------------------------
@@ -382,7 +388,10 @@ class Pipeline:
         the kernel as it reads the ranges; a ``RangeImage`` is taken as is, like
         the reference (a NaN or negative range is then simply no return).
         ``TimingRecord.ccl`` = device time of the fused kernel (every stage of
-        the reference runs inside it), ``total`` = wall time of the call.
+        the reference runs inside it), ``total`` = wall time of the call; with
+        ``stage_timing=True`` also ``ground`` / ``connectivity``: the device
+        times of those stages run on their own (extra launches, after the
+        fused one).
         """
         rec = TimingRecord()
         t0 = time.perf_counter()
@@ -410,6 +419,8 @@ class Pipeline:
             b["h_sz"].copy_(b["d_sz"], non_blocking=True)
             ev[2].record(s)
             ev[2].synchronize()
+        if self.stage_timing:
+            self._time_stages(b["d_in"], rec)
         k = int(b["h_ncl"][0])
         labels = b["h_lab"].numpy()[0].copy()
         if k == _native.RS_FRAME_INVALID:
@@ -421,6 +432,33 @@ class Pipeline:
         rec.total = (time.perf_counter() - t0) * 1e3
         return li, rec
 
+
+    def _time_stages(self, x: torch.Tensor, rec: TimingRecord):
+        """Device times of the reference's ground and connectivity stages run on
+        their own (the stage entries of the C ABI) for TimingRecord."""
+        H, W = self.shape
+        lib = _native.lib()
+        with torch.cuda.device(self.device):
+            s = torch.cuda.current_stream(self.device)
+            sp = ctypes.c_void_p(s.cuda_stream)
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+            z = torch.empty((1, H, W), dtype=torch.float32, device=self.device)
+            gm = torch.empty((1, H, W), dtype=torch.uint8, device=self.device)
+            hz = torch.empty((1, H, W), dtype=torch.uint8, device=self.device)
+            vt = torch.empty((1, max(H - 1, 0), W), dtype=torch.uint8, device=self.device)
+            cfg = ctypes.byref(self.rs_config)
+            tb = _ptr(self.device_tables())
+            ev[0].record(s)
+            if self.config.ground_removal:
+                _native.check(lib.rs_height_image(cfg, tb, _ptr(x), 1, _ptr(z), sp), "rs_height_image")
+            _native.check(lib.rs_ground_mask(cfg, tb, _ptr(x), _ptr(z), 1, _ptr(gm), sp), "rs_ground_mask")
+            ev[1].record(s)
+            _native.check(lib.rs_connectivity(cfg, tb, _ptr(x), _ptr(gm), 1, _ptr(hz), _ptr(vt), sp),
+                          "rs_connectivity")
+            ev[2].record(s)
+            ev[2].synchronize()
+        rec.ground = ev[0].elapsed_time(ev[1])
+        rec.connectivity = ev[1].elapsed_time(ev[2])
 
     # -- point clouds (pipeline.py:133-158) -------------------------------------
     def segment_clouds(self, clouds):

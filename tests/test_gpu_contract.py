@@ -223,3 +223,15 @@ def test_per_frame_api_equals_batch(cuda):
         assert np.array_equal(li.labels, want.labels)
         assert np.array_equal(li.cluster_sizes, want.cluster_sizes)
         assert rec.ccl > 0 and rec.total >= rec.ccl
+
+
+def test_stage_timing_record(cuda):
+    model = synthetic.sensor_for(synthetic.CONFIGS[0])
+    frame = synthetic.make_batch(0, 1, device="cpu").numpy()[0]
+    for ground in (True, False):
+        pipe = rs.Pipeline(model, rs.PipelineConfig(ground_removal=ground), device="cuda:0", stage_timing=True)
+        li, rec = pipe.segment_range_image(frame)
+        assert rec.ccl > 0 and rec.ground > 0 and rec.connectivity > 0
+        assert rec.total >= rec.ccl
+        wl, _ = oracle.segment_frame(frame, pipe.packed)
+        assert np.array_equal(li.labels, wl)
