@@ -744,6 +744,14 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
     }
 
     RS_MARK(7);
+    const bool axis = a.n_off > 0 && !a.planes;
+    if (axis) {
+        // ---- Map Connections of the skip offsets (0, k) / (k, 0), band-local,
+        // while the U plane is intact (rs_mc.cuh: mc_axis)
+        mc_axis(a, P, L, U, SB, NB, E, fr, r0, rows, tid, kFastThreads,
+                [&](uint32_t x, uint32_t y) { uf.unite(band | x, band | y); });
+        __syncthreads();   // U is read by mc_axis; X lists in it next
+    }
     // ---- X. cross-band unions over DSMEM -----------------------------------
     // Boundary edges are listed first (rows 1.. of the U plane are free now and
     // serve as the buffer), then united by all threads in parallel.  The up
@@ -826,7 +834,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
             return ((uint32_t)kt << a.SHN) | run_of(SBt, NBt, tw, tb);
         };
         if (!exp)
-            mc_runs(a, cl, k, P, L, SB, NB, fr, r0, rows, n_runs, tid, kFastThreads, ML, mcap, &ucur,
+            mc_runs(a, cl, k, P, L, SB, NB, fr, r0, rows, n_runs, tid, kFastThreads, ML, mcap, &ucur, axis,
                     [&](int kt, uint32_t id) { return kt == k ? E[id] : *cl.map_shared_rank(E + id, kt); },
                     [&](int kt, uint32_t id) { return uf.find_nc(((uint32_t)kt << a.SHN) | id); },
                     [&](uint32_t x, uint32_t y) { uf.unite_roots(x, y); });

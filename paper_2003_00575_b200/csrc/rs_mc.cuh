@@ -150,6 +150,117 @@ __device__ __forceinline__ int run_end(const uint32_t *Lrow, int cw, int b, int 
     return min(e, W - 1);
 }
 
+// Is offset o an axis offset the band-local fast path (mc_axis) takes?
+// (0, k): every row; (k, 0): the rows whose partner row lies in the band.
+__device__ __forceinline__ bool mc_axis_offset(const KArgs &a, int o) {
+    return (a.W & 31) == 0 && ((a.dy[o] == 0 && a.dx[o] > 0 && a.dx[o] < 32) || (a.dx[o] == 0 && a.dy[o] > 0));
+}
+
+// Axis-aligned Map Connections, band-local, right after barrier #1 (the
+// band's planes intact, its forest flat: E[run] = band-local root).  The
+// skip offsets of BASELINE's S, (0, k) and (k, 0), only ever join two runs
+// that the direct edges have not joined already when the cells between them
+// break the straight chain of links:
+//   (0, k): the pair is inside one run unless a run starts in (c - k, c] (or
+//           the pair crosses the seam, where runs end);
+//   (k, 0): rows r - k .. r are linked at column c by k up-edges unless one
+//           of the k U bits is clear.
+// Those candidate bits are word operations on the P / L / U / SB planes; of a
+// chain of candidates along the row whose own and partner cells are
+// left-linked (one run pair) only the first is kept.  A candidate whose runs
+// have different band-local roots is tested (the ranges from global memory)
+// and united.  (k, 0) rows whose partner row lies in another band are left
+// to step M.  `unite(x, y)` joins two own-band runs.
+template <class Unite>
+__device__ __forceinline__ void mc_axis(const KArgs &a, const uint32_t *P, const uint32_t *L, const uint32_t *U,
+                                        const uint32_t *SB, const uint32_t *NB, const uint32_t *E, const float *fr,
+                                        int r0, int rows, int tid, int nthreads, Unite unite) {
+    const int H = a.H, W = a.W, WPR = a.WPR;
+    const int nw = rows * WPR;
+    const float thr = a.dmax2;
+    for (int o = 0; o < a.n_off; ++o) {
+        if (!mc_axis_offset(a, o)) continue;
+        const int dy = a.dy[o], k = a.dx[o] ? a.dx[o] : dy;
+        const bool horiz = dy == 0;
+        // a thread per word (many independent words in flight)
+        for (int w = tid; w < nw; w += nthreads) {
+            const int q = divWPR(a, w), cw = w - q * WPR, r = r0 + q;
+            if (!horiz && q < dy) continue;   // partner row in another band: step M
+            const uint32_t pw = P[w];
+            if (!pw) continue;
+            uint32_t cand, ltw;
+            if (horiz) {
+                const int wl = cw > 0 ? w - 1 : w + WPR - 1;   // word to the left (the seam wraps)
+                const uint32_t pt = (pw << k) | (P[wl] >> (32 - k));
+                ltw = (L[w] << k) | (L[wl] >> (32 - k));
+                // a run start in (c - k, c]; across the seam runs always differ
+                const uint32_t sb = SB[w], sbl = SB[wl];
+                uint32_t diff = cw == 0 ? (1u << k) - 1u : 0u;
+                for (int i = 0; i < k; ++i) diff |= (sb << i) | (i ? sbl >> (32 - i) : 0u);
+                cand = pw & pt & diff;
+            } else {
+                ltw = L[w - dy * WPR];
+                uint32_t chain = ~0u;
+                for (int i = 0; i < dy; ++i) chain &= U[w - i * WPR];
+                cand = pw & P[w - dy * WPR] & ~chain;
+            }
+            if (!cand) continue;
+            // a chain (consecutive candidates whose own and partner cells are
+            // left-linked) joins one pair of runs: roots compared at its head
+            // (bit 0 of a word is always a head); the cells of chains whose
+            // roots differ are all tested (independent loads in flight), then
+            // each such chain unites at its first passing cell
+            const uint32_t heads = cand & ~((cand << 1) & L[w] & ltw);
+            const int tr = r - dy, tq = tr - r0;
+            uint32_t live = 0;   // cells of chains whose runs have different roots
+            for (uint32_t m = heads; m; m &= m - 1) {
+                const int b = __ffs(m) - 1;
+                int tc = cw * 32 + b - (horiz ? k : 0);
+                tc = tc < 0 ? tc + W : tc;
+                if (E[run_of(SB, NB, w, b)] == E[run_of(SB, NB, tq * WPR + (tc >> 5), tc & 31)]) continue;
+                // the chain: from b up to the next head
+                const uint32_t nxt = heads & ~lanemask_le(b);
+                const uint32_t upto = nxt ? ((1u << (__ffs(nxt) - 1)) - 1u) : ~0u;
+                live |= cand & upto & ~((1u << b) - 1u);
+            }
+            if (!live) continue;
+            const float tco = __ldg(a.tables + 6 * H - 5 + o * H + tr);
+            const float *orow = fr + (size_t)r * W, *trow = fr + (size_t)tr * W;
+            uint32_t pass = 0;
+            for (uint32_t m = live; m; ) {   // four cells per round: their loads overlap
+                float vo[4], vt[4];
+                int bb[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    bb[j] = m ? __ffs(m) - 1 : -1;
+                    if (m) m &= m - 1;
+                    vo[j] = vt[j] = 0.f;
+                    if (bb[j] >= 0) {
+                        const int c = cw * 32 + bb[j];
+                        int tc = c - (horiz ? k : 0);
+                        tc = tc < 0 ? tc + W : tc;
+                        vo[j] = __ldg(orow + c);
+                        vt[j] = __ldg(trow + tc);
+                    }
+                }
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    if (bb[j] >= 0 && pair_pass(vt[j], vo[j], tco, thr)) pass |= 1u << bb[j];
+            }
+            // first passing cell of each live chain: no passing cell before it in its chain
+            for (uint32_t m = pass; m; m &= m - 1) {
+                const int b = __ffs(m) - 1;
+                const uint32_t hb = heads & lanemask_le(b);
+                const int h = 31 - __clz(hb);
+                if (pass & ((1u << b) - 1u) & ~((1u << h) - 1u)) continue;
+                int tc = cw * 32 + b - (horiz ? k : 0);
+                tc = tc < 0 ? tc + W : tc;
+                unite(run_of(SB, NB, w, b), run_of(SB, NB, tq * WPR + (tc >> 5), tc & 31));
+            }
+        }
+    }
+}
+
 // Map Connections over RUNS (the production path of the fast kernel; the
 // cell-level mc_pass above serves the parity export and the overflow path).
 // Called by every thread of the CTA (it synchronises the CTA).
@@ -176,7 +287,8 @@ template <class Root, class Live, class Unite>
 __device__ __forceinline__ void mc_runs(const KArgs &a, const cg::cluster_group &cl, int k, const uint32_t *P,
                                         const uint32_t *L, const uint32_t *SB, const uint32_t *NB, const float *fr,
                                         int r0, int rows, uint32_t n_runs, int tid, int nthreads, uint32_t *list,
-                                        uint32_t cap, uint32_t *count, Root root, Live live, Unite unite) {
+                                        uint32_t cap, uint32_t *count, bool axis_done, Root root, Live live,
+                                        Unite unite) {
     const int H = a.H, W = a.W, R = a.R, WPR = a.WPR;
     const float thr = a.dmax2;
     const int nw = rows * WPR;
@@ -217,10 +329,18 @@ __device__ __forceinline__ void mc_runs(const KArgs &a, const cg::cluster_group 
         }
     };
     for (int o = 0; o < a.n_off; ++o) {
+        const int dy = a.dy[o], dx = a.dx[o];
+        // axis offsets done by mc_axis: none left for (0, k); for (k, 0) only
+        // the runs of rows q < dy (run ids follow cell order: ids below the
+        // first run of row dy)
+        uint32_t n_own = n_runs;
+        if (axis_done && mc_axis_offset(a, o)) {
+            if (dy == 0) continue;   // uniform: skips the round's barriers too
+            n_own = dy < rows ? NB[dy * WPR] : n_runs;
+        }
         if (tid == 0) *count = 0;
         __syncthreads();
-        const int dy = a.dy[o], dx = a.dx[o];
-        for (uint32_t own = tid; own < n_runs; own += nthreads) {
+        for (uint32_t own = tid; own < n_own; own += nthreads) {
             int lo = 0, hi = nw - 1;   // the word holding start `own`: the last w with NB[w] <= own
             while (lo < hi) {
                 const int mid = (lo + hi + 1) >> 1;
@@ -232,6 +352,7 @@ __device__ __forceinline__ void mc_runs(const KArgs &a, const cg::cluster_group 
             const int q = divWPR(a, w), cw = w - q * WPR, r = r0 + q;
             const int tr = r - dy;
             if (tr < 0) continue;
+            if (axis_done && mc_axis_offset(a, o) && (dy == 0 || q >= dy)) continue;   // done by mc_axis
             const int s = cw * 32 + b;
             const int e = run_end(L + q * WPR, cw, b, WPR, W);
             const uint32_t rown = root(k, own);
