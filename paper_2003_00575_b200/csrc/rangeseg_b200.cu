@@ -254,6 +254,17 @@ int make_plan_uncached(const rs_config *cfg, Plan *pl, int32_t batch) {
         fast_layout(Rf, W, (int)NC, &pl->kf);
         pl->kf.NC = (int)NC;
         pl->kf.udyn = pl->kf.C >= RS_UDYN_MIN_C;
+#ifdef RS_TMA_RING
+        {
+            // step A's TMA row ring: per warp up to RS_TMA_RING slots of 512 B in
+            // the union-find arrays (2 NC words), one mbarrier each in LR / KB
+            const long long by_ring = 2 * NC / (rs::kFastWarps * 128);
+            const long long by_bars = 2 * ((NC + 31) / 32) / (rs::kFastWarps * 2);
+            const int nst = (int)std::min<long long>({(long long)RS_TMA_RING, by_ring, by_bars});
+            const bool ok = W % 128 == 0 && W <= 128 * rs::kFastWarps && nst == RS_TMA_RING;   // one chunk task per warp
+            pl->kf.ring = ok ? nst : 0;
+        }
+#endif
         int SHN = 0;
         while ((1 << SHN) < NC) ++SHN;
         pl->kf.SHN = SHN;
@@ -310,16 +321,21 @@ int set_attrs(const Plan &pl) {
     if (dev != g_attr_device) {
         g_attr_device = dev;
         g_attr_smem_f = g_attr_smem_d = 0;
-        if ((st = cuda_check(cudaFuncSetAttribute(rs::rs_fast_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
+        if ((st = cuda_check(cudaFuncSetAttribute(rs::rs_fast_kernel<false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
                              "cudaFuncSetAttribute(fast, non-portable cluster)")) ||
+            (st = cuda_check(cudaFuncSetAttribute(rs::rs_fast_kernel<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
+                             "cudaFuncSetAttribute(fast + Map Connections, non-portable cluster)")) ||
             (st = cuda_check(cudaFuncSetAttribute(rs::rs_dense_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
                              "cudaFuncSetAttribute(dense, non-portable cluster)")))
             return st;
     }
     if (pl.fast && pl.smem_f > g_attr_smem_f) {
-        if ((st = cuda_check(cudaFuncSetAttribute(rs::rs_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        if ((st = cuda_check(cudaFuncSetAttribute(rs::rs_fast_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                   (int)std::max(pl.smem_f, (size_t)48 * 1024)),
-                             "cudaFuncSetAttribute(fast, smem)")))
+                             "cudaFuncSetAttribute(fast, smem)")) ||
+            (st = cuda_check(cudaFuncSetAttribute(rs::rs_fast_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                  (int)std::max(pl.smem_f, (size_t)48 * 1024)),
+                             "cudaFuncSetAttribute(fast + Map Connections, smem)")))
             return st;
         g_attr_smem_f = pl.smem_f;
     }
@@ -373,7 +389,13 @@ int segment_launch(const Plan &pl, const float *d_tables, const float *d_ranges,
     }
     k.stop_after = pl.stop_after;
     k.planes = d_planes;
-    return launch_cluster(rs::rs_fast_kernel, k, batch, rs::kFastThreads, pl.smem_f, stream, "rs_fast_kernel launch");
+    if ((reinterpret_cast<uintptr_t>(d_ranges) & 15u) != 0) k.ring = 0;   // bulk copies need 16-byte aligned rows
+    // two instantiations: frames without / with Map Connection offsets
+    if (k.n_off > 0)
+        return launch_cluster(rs::rs_fast_kernel<true>, k, batch, rs::kFastThreads, pl.smem_f, stream,
+                              "rs_fast_kernel<MC> launch");
+    return launch_cluster(rs::rs_fast_kernel<false>, k, batch, rs::kFastThreads, pl.smem_f, stream,
+                          "rs_fast_kernel launch");
 }
 
 // Output checks shared by the device and host entries (before any allocation

@@ -39,6 +39,7 @@ struct KArgs {
     int stop_after;               // experiments only (RS_EXPERIMENTS builds): leave the fast kernel after phase N
     uint32_t *planes;             // debug export (rs_fast_planes): the fast kernel's bit planes after step B, or NULL
     int udyn;                     // fast kernel: dynamic edge grabbing in the local unions (clusters of >= 2 bands)
+    int ring;                     // fast kernel (RS_TMA_RING builds): slots of each warp's TMA row ring in step A, 0 = off
 };
 
 // ------------------------------------------------------------ phase markers
@@ -240,6 +241,13 @@ __device__ __forceinline__ uint32_t smem_addr(const void *p) {
 __device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
     uint32_t v;
     asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+
+// ordered against the mbarrier waits of the TMA row ring (never hoisted or merged)
+__device__ __forceinline__ uint32_t lds_u32v(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
     return v;
 }
 

@@ -191,7 +191,7 @@ struct RunUF {
 // 16-byte stores of the four words by lane 0).  GROUND: ground removal on.
 // Plane stores use 32-bit shared-memory byte addresses (sP/sL/sU: the chunk's
 // words in the band's first row; sPh/sLh: the halo row).
-template <bool FULL, bool GROUND>
+template <bool FULL, bool GROUND, bool RING = false>
 struct BitsStrip {
     const KArgs &a;
     const float *col;
@@ -227,7 +227,7 @@ struct BitsStrip {
     template <bool ROW0, bool HALO = false>
     __device__ __forceinline__ void step(int r, const float (&va)[4], const float (&v)[4], const float (&vb)[4],
                                          float (&vn)[4]) const {
-        if (!ROW0) {   // prefetch row r + RS_STRIP_SETS - 2
+        if (!ROW0 && !RING) {   // prefetch row r + RS_STRIP_SETS - 2
             ldp(np, vn, r + RS_STRIP_SETS - 2 < rend);
             np += rowf;
         }
@@ -275,6 +275,104 @@ struct BitsStrip {
             if (!halo) sts32(sU + lo, xu);
         }
     }
+
+#ifdef RS_TMA_RING
+    // ---- TMA row ring (RS_TMA_RING builds; FULL chunks only) -----------------
+    // The warp's 512-byte row segments are staged by 1-D bulk copies
+    // (cp.async.bulk, issued by lane 0, completion on a per-slot mbarrier)
+    // into a private ring of `nst` slots in the idle union-find arrays, up to
+    // nst rows ahead of the walk.  The step's ranges come from shared memory
+    // (conflict-free 4-byte loads at 32 j + lane), so only the row above and
+    // the current row live in registers (two sets instead of four).  A slot is
+    // refilled by the warp itself after the step that consumed its row (the
+    // ballots depend on the values, so the loads have completed): no
+    // consumer-release barrier is needed.
+    uint32_t ring = 0;      // shared-memory byte address of the warp's ring (+ 4 lane)
+    uint32_t bars = 0;      // shared-memory byte address of the warp's mbarriers
+    static constexpr int kSt = RS_TMA_RING;   // slots (a power of two)
+    static_assert((kSt & (kSt - 1)) == 0 && kSt >= 2, "RS_TMA_RING must be a power of two");
+    mutable uint32_t ci = 0;            // rows fetched so far: slot = ci % kSt, parity = (ci / kSt) & 1
+    mutable int pnext = 0;              // next row to issue
+    mutable const float *gsrc = nullptr;   // its chunk segment in global memory
+
+    // lane 0: row pnext -> the slot of fetch number i (i % kSt)
+    __device__ __forceinline__ void issue(uint32_t i) const {
+        if (pnext < rend && lane == 0) {
+            const uint32_t s = i & (kSt - 1);
+            const uint32_t bar = bars + 8u * s, dst = ring + 512u * s;
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], 512;" ::"r"(bar) : "memory");
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 512, [%2];" ::"r"(dst),
+                         "l"(gsrc), "r"(bar)
+                         : "memory");
+        }
+        ++pnext;
+        gsrc += rowf;
+    }
+    // Rows are fetched strictly in order.  Before waiting for fetch ci the slot
+    // of fetch ci - 1 is refilled: its values were consumed by the previous
+    // step (or, for the very first rows, are refilled one fetch later).
+    template <bool REFILL = true>
+    __device__ __forceinline__ void get(float (&x)[4]) const {
+        if (REFILL) issue(ci - 1u);
+        const uint32_t s = ci & (kSt - 1);
+        const uint32_t bar = bars + 8u * s;
+        const uint32_t par = (ci / kSt) & 1u;
+        uint32_t done = 0;
+        while (!done) {
+            asm volatile(
+                "{\n\t.reg .pred p;\n\t"
+                "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                "selp.u32 %0, 1, 0, p;\n\t}"
+                : "=r"(done)
+                : "r"(bar), "r"(par)
+                : "memory");
+        }
+        const uint32_t src = ring + 512u * s + 4u * (uint32_t)lane;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) x[j] = __uint_as_float(lds_u32v(src + 128u * j));
+        ++ci;
+    }
+
+    __device__ __forceinline__ void run_ring() const {
+        float S0[4], S1[4];
+        const int first = rfirst == 0 ? 0 : rfirst - 1;
+        pnext = first;
+        gsrc = col - lane + (size_t)first * rowf;
+        ci = 0;
+#pragma unroll 1
+        for (uint32_t i = 0; i < (uint32_t)kSt; ++i) issue(i);
+        int r;
+        // the first two fetches are consumed by the first step: their slots are
+        // refilled after it (fetch 0 by the next get, fetch 1 by the one after)
+        get<false>(S0);
+        if (rfirst == 0) {   // row 0: ground pair (0, 1), no up edges
+            if (1 < rend) get<false>(S1);
+            else {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) S1[j] = 0.f;
+            }
+            if (r0 > 0) step<true, true>(0, S0, S0, S1, S0);
+            else step<true>(0, S0, S0, S1, S0);
+            if (1 >= rend) return;
+            issue(0u);
+            step<false>(1, S0, S1, S1, S0);
+            r = 2;   // row above = S1
+        } else {
+            get<false>(S1);
+            if (rfirst < r0) step<false, true>(rfirst, S0, S1, S1, S0);   // the halo row: P / L only
+            else step<false>(rfirst, S0, S1, S1, S0);
+            issue(0u);
+            r = rfirst + 1;   // row above = S1
+        }
+        for (; r < rend; r += 2) {
+            get(S0);
+            step<false>(r, S1, S0, S0, S1);
+            if (r + 1 >= rend) break;
+            get(S1);
+            step<false>(r + 1, S0, S1, S1, S0);
+        }
+    }
+#endif
 
 #if RS_STRIP_SETS == 3
     // three rotating sets: rows r-1, r and the target of the one-row prefetch
@@ -362,6 +460,10 @@ struct BitsStrip {
 #endif
 };
 
+// MC: the frame has Map Connection offsets (a.n_off > 0).  A separate
+// instantiation, so the code generation of the default kernel (whose speed is
+// sensitive to register allocation) does not depend on the Map Connection code.
+template <bool MC>
 __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const __grid_constant__ KArgs a) {
     extern __shared__ __align__(128) uint32_t sm[];
     __shared__ uint32_t warp_tot[kFastWarps];
@@ -419,6 +521,19 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
         const int nrow = rend - rstart;
         const int S = max(1, min(kFastWarps / nchunk, nrow / 8));
         const int per = (nrow + S - 1) / S;
+#ifdef RS_TMA_RING
+        // the warp's row ring (idle union-find arrays) and its mbarriers (idle LR / KB words)
+        const uint32_t ring_base = smem_addr(sm + a.o_E) + 512u * (uint32_t)(warp * RS_TMA_RING);
+        const uint32_t bars_base = smem_addr(sm + a.o_LR) + 8u * (uint32_t)(warp * RS_TMA_RING);
+        if (a.ring) {
+            if (lane == 0) {
+                for (int i = 0; i < RS_TMA_RING; ++i)
+                    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bars_base + 8u * (uint32_t)i) : "memory");
+                asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            }
+            __syncwarp();
+        }
+#endif
         for (int t = warp; t < nchunk * S; t += kFastWarps) {
             const int ch = t % nchunk, part = t / nchunk;
             const int rlo = rstart + part * per, rhi = min(rend, rlo + per);
@@ -434,6 +549,22 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
         st.run();                                                                                           \
         umx = max(umx, st.mx);                                                                              \
     } while (0)
+#ifdef RS_TMA_RING
+#define RS_RING(G)                                                                                              \
+    do {                                                                                                    \
+        BitsStrip<true, G, true> st{a, fr + cb, rowc, sP, sL, sU, sPh, sLh, ch, lane, r0, rstart, rhi, cb, thr, \
+                                    tch, rlo, W, 4 * WPR};                                                  \
+        st.ring = ring_base;                                                                                \
+        st.bars = bars_base;                                                                                \
+        st.run_ring();                                                                                      \
+        umx = max(umx, st.mx);                                                                              \
+    } while (0)
+            if (a.ring && full) {
+                if (a.ground) RS_RING(true); else RS_RING(false);
+                continue;
+            }
+#undef RS_RING
+#endif
             if (a.ground) {
                 if (full) RS_STRIP(true, true); else RS_STRIP(false, true);
             } else {
@@ -441,6 +572,11 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
             }
 #undef RS_STRIP
         }
+#ifdef RS_TMA_RING
+        if (a.ring && lane == 0)
+            for (int i = 0; i < RS_TMA_RING; ++i)
+                asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(bars_base + 8u * (uint32_t)i) : "memory");
+#endif
         if (__any_sync(kFull, umx > kMaxFiniteBits) && lane == 0) cta_bad = 1u;
     }
     __syncthreads();
@@ -671,25 +807,54 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
         RS_MARK(4);
     RS_STOP(3);
         // local flatten; LR marks the band-local roots
-        for (uint32_t base = warp * 32; base < n_runs; base += kFastThreads) {
-            const uint32_t id = base + lane;
-            bool lr = false;
-            if (id < n_runs) {
-                // most trees are at most two deep after the unions: two plain
-                // loads, then (rarely) path halving with atomicMin — entries only
-                // ever decrease, so a finished root pointer is never overwritten
-                const uint32_t p = E[id];
-                const uint32_t gp = E[p & maskN];
-                const uint32_t r = gp == p ? p : uf.find_local_min(gp);
-                E[id] = r;
-                SZ[id] = 0;   // it served as the edge list
-                lr = r == (band | id);
+        auto flatten = [&]() {
+            for (uint32_t base = warp * 32; base < n_runs; base += kFastThreads) {
+                const uint32_t id = base + lane;
+                bool lr = false;
+                if (id < n_runs) {
+                    // most trees are at most two deep after the unions: two plain
+                    // loads, then (rarely) path halving with atomicMin — entries only
+                    // ever decrease, so a finished root pointer is never overwritten
+                    const uint32_t p = E[id];
+                    const uint32_t gp = E[p & maskN];
+                    const uint32_t r = gp == p ? p : uf.find_local_min(gp);
+                    E[id] = r;
+                    SZ[id] = 0;   // it served as the edge list
+                    lr = r == (band | id);
+                }
+                const uint32_t m = __ballot_sync(kFull, lr);
+                if (lane == 0) LR[base >> 5] = m;
             }
-            const uint32_t m = __ballot_sync(kFull, lr);
-            if (lane == 0) LR[base >> 5] = m;
-        }
+        };
+        flatten();
+        if (MC && tid == 0) n_edges = 0;
         __syncthreads();
         RS_MARK(5);
+        if (MC && a.n_off > 0 && !a.planes) {
+            // ---- Map Connections of the skip offsets (0, k) / (k, 0) inside the
+            // band (rs_mc.cuh: mc_axis_list / mc_axis_unite), while nothing
+            // outside the CTA touches its forest: candidate cells whose runs
+            // have different local roots are listed (the size array is the
+            // buffer), then tested and united by all threads, and the forest
+            // is flattened again.  Rows whose partner row lies in another band
+            // are handled with the cross-band edges (step X).
+            const uint32_t lcap = (uint32_t)a.NC;
+            auto test_unite = [&](uint32_t e) {
+                mc_axis_cell(a, SB, NB, fr, r0, e, [&](uint32_t x, uint32_t y) { uf.unite_local(band | x, band | y); });
+            };
+            mc_axis_list(a, P, L, U, SB, NB, E, r0, rows, tid, kFastThreads, SZ, lcap, &n_edges, test_unite);
+            __syncthreads();
+            RS_MARK(21);
+            const uint32_t nl = min(n_edges, lcap);   // block-uniform
+            if (n_edges) {
+                for (uint32_t i = tid; i < nl; i += kFastThreads) test_unite(SZ[i]);
+                __syncthreads();
+                for (uint32_t i = tid; i < nl; i += kFastThreads) SZ[i] = 0;
+                flatten();
+                __syncthreads();
+            }
+            RS_MARK(22);
+        }
         // local component sizes: each run adds its length to its local root
         int carry = INT_MAX;   // first run end after the current chunk
         const int nchunks = (wr1 - wr0 + 31) / 32;
@@ -744,13 +909,15 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
     }
 
     RS_MARK(7);
-    const bool axis = a.n_off > 0 && !a.planes;
+    // Map Connections: the skip offsets (0, k) / (k, 0) were united inside the
+    // band before barrier #1 and are finished with the cross-band edges below;
+    // step M is only needed for other offsets (and for the parity export)
+    const bool axis = MC && a.n_off > 0 && !a.planes;
+    bool mstep = MC && a.n_off > 0;
     if (axis) {
-        // ---- Map Connections of the skip offsets (0, k) / (k, 0), band-local,
-        // while the U plane is intact (rs_mc.cuh: mc_axis)
-        mc_axis(a, P, L, U, SB, NB, E, fr, r0, rows, tid, kFastThreads,
-                [&](uint32_t x, uint32_t y) { uf.unite(band | x, band | y); });
-        __syncthreads();   // U is read by mc_axis; X lists in it next
+        bool all_axis = true;
+        for (int o = 0; o < a.n_off; ++o) all_axis &= mc_axis_offset(a, o);
+        mstep = !all_axis;
     }
     // ---- X. cross-band unions over DSMEM -----------------------------------
     // Boundary edges are listed first (rows 1.. of the U plane are free now and
@@ -804,6 +971,9 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
         const int whalf = WPR / 2;
         if (r0 > 0) boundary(k, whalf, WPR);
         if (k + 1 < a.C) boundary(k + 1, 0, whalf);
+        // (k, 0) Map Connection pairs whose partner row lies in a band above:
+        // a lane per cell, passing pairs join the cross-band edge list
+        if (axis && r0 > 0) mc_axis_cross(a, cl, k, P, L, SB, NB, fr, r0, rows, lane, warp, kFastWarps, xpush);
         __syncthreads();
         const uint32_t nx = min(n_xedges, xcap);
         for (uint32_t e = tid; e < nx; e += kFastThreads) uf.unite(XL[2 * e], XL[2 * e + 1]);
@@ -813,7 +983,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
     cl.sync();   // #2: the forest of the direct edges is final
     RS_MARK(9);
 #ifndef RS_MC_NO_PASS
-    if (a.n_off > 0) {
+    if (mstep) {
         // ---- M. Map Connection edges (rs_mc.cuh).  Every run first points
         // straight at its root (a compression of the final direct-edge forest;
         // other bands may still be compressing, which only makes a root
@@ -971,7 +1141,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
             // lr: the band-local root (E[lr] = the final root after Z), or
             // with Map Connections the root before step M (a local root of
             // its band: one hop, possibly over DSMEM, to the final root)
-            const uint32_t g = ((lr >> a.SHN) == (uint32_t)k) ? E[lr & maskN] : (a.n_off ? uf.ld(lr) : lr);
+            const uint32_t g = ((lr >> a.SHN) == (uint32_t)k) ? E[lr & maskN] : (mstep ? uf.ld(lr) : lr);
             const int owner = (int)(g >> a.SHN);
             const uint32_t gi = g & maskN;
             uint32_t km, wk;

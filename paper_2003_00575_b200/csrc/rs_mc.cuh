@@ -156,36 +156,38 @@ __device__ __forceinline__ bool mc_axis_offset(const KArgs &a, int o) {
     return (a.W & 31) == 0 && ((a.dy[o] == 0 && a.dx[o] > 0 && a.dx[o] < 32) || (a.dx[o] == 0 && a.dy[o] > 0));
 }
 
-// Axis-aligned Map Connections, band-local, right after barrier #1 (the
-// band's planes intact, its forest flat: E[run] = band-local root).  The
-// skip offsets of BASELINE's S, (0, k) and (k, 0), only ever join two runs
-// that the direct edges have not joined already when the cells between them
-// break the straight chain of links:
+// Axis-aligned Map Connections (BASELINE's skip offsets (0, k) and (k, 0)).
+// They only ever join two runs that the direct edges have not joined already
+// when the cells between them break the straight chain of links:
 //   (0, k): the pair is inside one run unless a run starts in (c - k, c] (or
 //           the pair crosses the seam, where runs end);
 //   (k, 0): rows r - k .. r are linked at column c by k up-edges unless one
 //           of the k U bits is clear.
-// Those candidate bits are word operations on the P / L / U / SB planes; of a
-// chain of candidates along the row whose own and partner cells are
-// left-linked (one run pair) only the first is kept.  A candidate whose runs
-// have different band-local roots is tested (the ranges from global memory)
-// and united.  (k, 0) rows whose partner row lies in another band are left
-// to step M.  `unite(x, y)` joins two own-band runs.
-template <class Unite>
-__device__ __forceinline__ void mc_axis(const KArgs &a, const uint32_t *P, const uint32_t *L, const uint32_t *U,
-                                        const uint32_t *SB, const uint32_t *NB, const uint32_t *E, const float *fr,
-                                        int r0, int rows, int tid, int nthreads, Unite unite) {
-    const int H = a.H, W = a.W, WPR = a.WPR;
+// Those candidate bits are word operations on the P / L / U / SB planes.
+//
+// mc_axis_list (inside the band, after the local flatten: E[run] = band-local
+// root): a thread per word; of a chain of candidates along the row whose own
+// and partner cells are left-linked (one run pair) the roots are compared once,
+// at its head; the cells of chains whose roots differ are LISTED (entry =
+// word | bit << 16 | offset << 21).  The caller then gives every listed cell
+// to a thread (mc_axis_cell: two ranges from global memory, the pair test, a
+// union on a pass), so the loads and unions are spread evenly over the CTA
+// whatever the words look like.  A full list falls back to `now(entry)`.
+// (k, 0) rows whose partner row lies in another band: mc_axis_cross.
+template <class Now>
+__device__ __forceinline__ void mc_axis_list(const KArgs &a, const uint32_t *P, const uint32_t *L, const uint32_t *U,
+                                             const uint32_t *SB, const uint32_t *NB, const uint32_t *E, int r0,
+                                             int rows, int tid, int nthreads, uint32_t *list, uint32_t cap,
+                                             uint32_t *count, Now now) {
+    const int W = a.W, WPR = a.WPR;
     const int nw = rows * WPR;
-    const float thr = a.dmax2;
     for (int o = 0; o < a.n_off; ++o) {
         if (!mc_axis_offset(a, o)) continue;
         const int dy = a.dy[o], k = a.dx[o] ? a.dx[o] : dy;
         const bool horiz = dy == 0;
-        // a thread per word (many independent words in flight)
         for (int w = tid; w < nw; w += nthreads) {
-            const int q = divWPR(a, w), cw = w - q * WPR, r = r0 + q;
-            if (!horiz && q < dy) continue;   // partner row in another band: step M
+            const int q = divWPR(a, w), cw = w - q * WPR;
+            if (q < dy) continue;   // partner row in another band (or above the frame)
             const uint32_t pw = P[w];
             if (!pw) continue;
             uint32_t cand, ltw;
@@ -205,58 +207,89 @@ __device__ __forceinline__ void mc_axis(const KArgs &a, const uint32_t *P, const
                 cand = pw & P[w - dy * WPR] & ~chain;
             }
             if (!cand) continue;
-            // a chain (consecutive candidates whose own and partner cells are
-            // left-linked) joins one pair of runs: roots compared at its head
-            // (bit 0 of a word is always a head); the cells of chains whose
-            // roots differ are all tested (independent loads in flight), then
-            // each such chain unites at its first passing cell
-            const uint32_t heads = cand & ~((cand << 1) & L[w] & ltw);
-            const int tr = r - dy, tq = tr - r0;
+            const uint32_t heads = cand & ~((cand << 1) & L[w] & ltw);   // bit 0 of a word is always a head
+            const int tqw = (q - dy) * WPR;
             uint32_t live = 0;   // cells of chains whose runs have different roots
             for (uint32_t m = heads; m; m &= m - 1) {
                 const int b = __ffs(m) - 1;
                 int tc = cw * 32 + b - (horiz ? k : 0);
                 tc = tc < 0 ? tc + W : tc;
-                if (E[run_of(SB, NB, w, b)] == E[run_of(SB, NB, tq * WPR + (tc >> 5), tc & 31)]) continue;
-                // the chain: from b up to the next head
-                const uint32_t nxt = heads & ~lanemask_le(b);
+                if (E[run_of(SB, NB, w, b)] == E[run_of(SB, NB, tqw + (tc >> 5), tc & 31)]) continue;
+                const uint32_t nxt = heads & ~lanemask_le(b);   // the chain: from b up to the next head
                 const uint32_t upto = nxt ? ((1u << (__ffs(nxt) - 1)) - 1u) : ~0u;
                 live |= cand & upto & ~((1u << b) - 1u);
             }
             if (!live) continue;
-            const float tco = __ldg(a.tables + 6 * H - 5 + o * H + tr);
-            const float *orow = fr + (size_t)r * W, *trow = fr + (size_t)tr * W;
-            uint32_t pass = 0;
-            for (uint32_t m = live; m; ) {   // four cells per round: their loads overlap
-                float vo[4], vt[4];
-                int bb[4];
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    bb[j] = m ? __ffs(m) - 1 : -1;
-                    if (m) m &= m - 1;
-                    vo[j] = vt[j] = 0.f;
-                    if (bb[j] >= 0) {
-                        const int c = cw * 32 + bb[j];
-                        int tc = c - (horiz ? k : 0);
-                        tc = tc < 0 ? tc + W : tc;
-                        vo[j] = __ldg(orow + c);
-                        vt[j] = __ldg(trow + tc);
-                    }
-                }
-#pragma unroll
-                for (int j = 0; j < 4; ++j)
-                    if (bb[j] >= 0 && pair_pass(vt[j], vo[j], tco, thr)) pass |= 1u << bb[j];
+            uint32_t slot = atomicAdd(count, (uint32_t)__popc(live));
+            for (uint32_t m = live; m; m &= m - 1, ++slot) {
+                const uint32_t e = (uint32_t)w | ((uint32_t)(__ffs(m) - 1) << 16) | ((uint32_t)o << 21);
+                if (slot < cap) list[slot] = e;
+                else now(e);
             }
-            // first passing cell of each live chain: no passing cell before it in its chain
-            for (uint32_t m = pass; m; m &= m - 1) {
-                const int b = __ffs(m) - 1;
-                const uint32_t hb = heads & lanemask_le(b);
-                const int h = 31 - __clz(hb);
-                if (pass & ((1u << b) - 1u) & ~((1u << h) - 1u)) continue;
-                int tc = cw * 32 + b - (horiz ? k : 0);
-                tc = tc < 0 ? tc + W : tc;
-                unite(run_of(SB, NB, w, b), run_of(SB, NB, tq * WPR + (tc >> 5), tc & 31));
+        }
+    }
+}
+
+// One listed cell of mc_axis_list: test the pair, `unite(x, y)` (run ids of the band) on a pass.
+template <class Unite>
+__device__ __forceinline__ void mc_axis_cell(const KArgs &a, const uint32_t *SB, const uint32_t *NB, const float *fr,
+                                             int r0, uint32_t e, Unite unite) {
+    const int W = a.W, WPR = a.WPR, H = a.H;
+    const int w = (int)(e & 0xffffu), b = (int)((e >> 16) & 31u), o = (int)(e >> 21);
+    const int dy = a.dy[o], dx = a.dx[o];
+    const int q = divWPR(a, w), cw = w - q * WPR;
+    const int r = r0 + q, tr = r - dy, c = cw * 32 + b;
+    int tc = c - dx;
+    tc = tc < 0 ? tc + W : tc;
+    const float vo = __ldg(fr + (size_t)r * W + c), vt = __ldg(fr + (size_t)tr * W + tc);
+    const float tco = __ldg(a.tables + 6 * H - 5 + o * H + tr);
+    if (pair_pass(vt, vo, tco, a.dmax2))
+        unite(run_of(SB, NB, w, b), run_of(SB, NB, (q - dy) * WPR + (tc >> 5), tc & 31));
+}
+
+// (k, 0) pairs whose partner row lies in a band above (the first k rows of
+// the band): a lane per cell.  The other band's P / L / SB / NB planes are
+// read over DSMEM (final since step R; its U plane is not — the band may
+// already be listing cross-band edges in it — so every present pair is
+// tested: any passing pair may be united at any time, the components are
+// those of the graph of all passing edges).  Of consecutive passing pairs
+// whose own and partner cells are left-linked only the first is pushed.
+// push(has, x, y) is called by every lane (band-tagged run ids).
+template <class Push>
+__device__ __forceinline__ void mc_axis_cross(const KArgs &a, const cg::cluster_group &cl, int kb, const uint32_t *P,
+                                              const uint32_t *L, const uint32_t *SB, const uint32_t *NB,
+                                              const float *fr, int r0, int rows, int lane, int warp, int nwarps,
+                                              Push push) {
+    const int W = a.W, WPR = a.WPR, R = a.R, H = a.H;
+    const uint32_t own_tag = (uint32_t)kb << a.SHN;
+    for (int o = 0; o < a.n_off; ++o) {
+        if (!mc_axis_offset(a, o) || a.dy[o] == 0) continue;
+        const int dy = a.dy[o];
+        const int nq = min(dy, rows);
+        for (int wi = warp; wi < nq * WPR; wi += nwarps) {   // a warp per word (W % 32 == 0)
+            const int q = wi / WPR, cw = wi - q * WPR;
+            const int r = r0 + q, tr = r - dy;
+            if (tr < 0) continue;   // warp-uniform
+            const int kt = tr / R, tq = tr - kt * R;
+            const int w = q * WPR + cw, tw = tq * WPR + cw;
+            const uint32_t *Pp = cl.map_shared_rank(P, kt), *Lp = cl.map_shared_rank(L, kt);
+            const uint32_t both = P[w] & Pp[tw];
+            if (!both) continue;   // warp-uniform
+            const bool mine = (both >> lane) & 1u;
+            const int c = cw * 32 + lane;
+            bool pass = false;
+            if (mine)
+                pass = pair_pass(__ldg(fr + (size_t)tr * W + c), __ldg(fr + (size_t)r * W + c),
+                                 __ldg(a.tables + 6 * H - 5 + o * H + tr), a.dmax2);
+            const uint32_t m = __ballot_sync(kFull, pass);
+            const uint32_t dup = (m << 1) & L[w] & Lp[tw];   // the pair to the left passed and joins the same runs
+            const bool has = pass && !((dup >> lane) & 1u);
+            uint32_t x = 0, y = 0;
+            if (has) {
+                x = own_tag | run_of(SB, NB, w, lane);
+                y = ((uint32_t)kt << a.SHN) | run_of(cl.map_shared_rank(SB, kt), cl.map_shared_rank(NB, kt), tw, lane);
             }
+            push(has, x, y);
         }
     }
 }
@@ -333,11 +366,9 @@ __device__ __forceinline__ void mc_runs(const KArgs &a, const cg::cluster_group 
         // axis offsets done by mc_axis: none left for (0, k); for (k, 0) only
         // the runs of rows q < dy (run ids follow cell order: ids below the
         // first run of row dy)
-        uint32_t n_own = n_runs;
-        if (axis_done && mc_axis_offset(a, o)) {
-            if (dy == 0) continue;   // uniform: skips the round's barriers too
-            n_own = dy < rows ? NB[dy * WPR] : n_runs;
-        }
+        // axis offsets were done by mc_axis (every row, cross-band rows included)
+        if (axis_done && mc_axis_offset(a, o)) continue;   // uniform: skips the round's barriers too
+        const uint32_t n_own = n_runs;
         if (tid == 0) *count = 0;
         __syncthreads();
         for (uint32_t own = tid; own < n_own; own += nthreads) {
@@ -352,7 +383,6 @@ __device__ __forceinline__ void mc_runs(const KArgs &a, const cg::cluster_group 
             const int q = divWPR(a, w), cw = w - q * WPR, r = r0 + q;
             const int tr = r - dy;
             if (tr < 0) continue;
-            if (axis_done && mc_axis_offset(a, o) && (dy == 0 || q >= dy)) continue;   // done by mc_axis
             const int s = cw * 32 + b;
             const int e = run_end(L + q * WPR, cw, b, WPR, W);
             const uint32_t rown = root(k, own);
