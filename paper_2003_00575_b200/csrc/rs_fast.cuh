@@ -832,25 +832,59 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
         RS_MARK(5);
         if (MC && a.n_off > 0 && !a.planes) {
             // ---- Map Connections of the skip offsets (0, k) / (k, 0) inside the
-            // band (rs_mc.cuh: mc_axis_list / mc_axis_unite), while nothing
-            // outside the CTA touches its forest: candidate cells whose runs
-            // have different local roots are listed (the size array is the
-            // buffer), then tested and united by all threads, and the forest
-            // is flattened again.  Rows whose partner row lies in another band
+            // band (rs_mc.cuh: mc_axis_heads / mc_axis_chain), while nothing
+            // outside the CTA touches its forest: chains of candidate pairs whose
+            // runs have different local roots are listed (the size array is
+            // the buffer), then tested and united by all threads, and the
+            // forest is flattened again.  Rows whose partner row lies in another band
             // are handled with the cross-band edges (step X).
-            const uint32_t lcap = (uint32_t)a.NC;
-            auto test_unite = [&](uint32_t e) {
-                mc_axis_cell(a, SB, NB, fr, r0, e, [&](uint32_t x, uint32_t y) { uf.unite_local(band | x, band | y); });
+            const uint32_t lcap = (uint32_t)a.NC / 2u;   // two words per chain
+            auto chain = [&](uint32_t e, uint32_t cells) {
+                mc_axis_chain(a, P, L, U, SB, NB, fr, r0, e, cells,
+                              [&](uint32_t x, uint32_t y) { uf.unite_local(band | x, band | y); });
             };
-            mc_axis_list(a, P, L, U, SB, NB, E, r0, rows, tid, kFastThreads, SZ, lcap, &n_edges, test_unite);
+            mc_axis_heads(a, P, L, U, SB, NB, E, rows, tid, kFastThreads, SZ, lcap, &n_edges, chain);
             __syncthreads();
+            const uint32_t nl = min(n_edges, lcap);
+            const bool any = nl != 0u;   // block-uniform
+            for (uint32_t i = tid; i < nl; i += kFastThreads) {
+                const uint32_t e = SZ[2 * i], cells = SZ[2 * i + 1];
+                SZ[2 * i] = SZ[2 * i + 1] = 0;
+                chain(e, cells);
+            }
             RS_MARK(21);
-            const uint32_t nl = min(n_edges, lcap);   // block-uniform
-            if (n_edges) {
-                for (uint32_t i = tid; i < nl; i += kFastThreads) test_unite(SZ[i]);
+            if (any) {
+                // flatten again, in two steps: the roots of the first flatten
+                // (LR bits; every other run points at one of them) find their
+                // new root, then every run takes one hop
                 __syncthreads();
-                for (uint32_t i = tid; i < nl; i += kFastThreads) SZ[i] = 0;
-                flatten();
+                // (pointer jumping: every such root repeats E[r] = E[E[r]] while
+                // the others do the same, so a chain of hooks of any depth —
+                // skips merge runs along a row one after the other — takes a
+                // logarithmic number of steps)
+                for (uint32_t w = warp; w < (n_runs + 31) / 32; w += kFastWarps) {
+                    const uint32_t id = w * 32 + lane;
+                    if (!((LR[w] >> lane) & 1u)) continue;
+                    volatile uint32_t *V = E;
+                    while (true) {
+                        const uint32_t p = V[id];
+                        const uint32_t gp = V[p & maskN];
+                        if (gp == p) break;
+                        V[id] = gp;
+                    }
+                }
+                __syncthreads();
+                for (uint32_t base = warp * 32; base < n_runs; base += kFastThreads) {
+                    const uint32_t id = base + lane;
+                    bool lr = false;
+                    if (id < n_runs) {
+                        const uint32_t r = E[E[id] & maskN];
+                        E[id] = r;
+                        lr = r == (band | id);
+                    }
+                    const uint32_t m = __ballot_sync(kFull, lr);
+                    if (lane == 0) LR[base >> 5] = m;
+                }
                 __syncthreads();
             }
             RS_MARK(22);
@@ -972,8 +1006,12 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
         if (r0 > 0) boundary(k, whalf, WPR);
         if (k + 1 < a.C) boundary(k + 1, 0, whalf);
         // (k, 0) Map Connection pairs whose partner row lies in a band above:
-        // a lane per cell, passing pairs join the cross-band edge list
-        if (axis && r0 > 0) mc_axis_cross(a, cl, k, P, L, SB, NB, fr, r0, rows, lane, warp, kFastWarps, xpush);
+        // a lane per cell, passing pairs join the cross-band edge list; shared
+        // by the two bands of a boundary like the up edges
+        if (axis) {
+            if (r0 > 0) mc_axis_cross(a, cl, k, k, P, L, SB, NB, fr, lane, warp, kFastWarps, xpush);
+            if (k + 1 < a.C) mc_axis_cross(a, cl, k, k + 1, P, L, SB, NB, fr, lane, warp, kFastWarps, xpush);
+        }
         __syncthreads();
         const uint32_t nx = min(n_xedges, xcap);
         for (uint32_t e = tid; e < nx; e += kFastThreads) uf.unite(XL[2 * e], XL[2 * e + 1]);

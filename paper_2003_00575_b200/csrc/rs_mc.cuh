@@ -165,131 +165,207 @@ __device__ __forceinline__ bool mc_axis_offset(const KArgs &a, int o) {
 //           of the k U bits is clear.
 // Those candidate bits are word operations on the P / L / U / SB planes.
 //
-// mc_axis_list (inside the band, after the local flatten: E[run] = band-local
-// root): a thread per word; of a chain of candidates along the row whose own
-// and partner cells are left-linked (one run pair) the roots are compared once,
-// at its head; the cells of chains whose roots differ are LISTED (entry =
-// word | bit << 16 | offset << 21).  The caller then gives every listed cell
-// to a thread (mc_axis_cell: two ranges from global memory, the pair test, a
-// union on a pass), so the loads and unions are spread evenly over the CTA
-// whatever the words look like.  A full list falls back to `now(entry)`.
-// (k, 0) rows whose partner row lies in another band: mc_axis_cross.
+// Inside the band (after the local flatten: E[run] = band-local root).
+// mc_axis_heads: a thread per word; a chain of candidates along the row whose
+// own and partner cells are left-linked joins one pair of runs, so the roots
+// are compared once, at its head (bit 0 of a word is always a head), and the
+// heads whose roots differ are LISTED (entry = word | bit << 16 | offset <<
+// 21, and the chain's cell bits: two words, `cap` entries).  The caller then
+// gives every listed head to a thread (mc_axis_chain):
+// the chain's cells are tested (ranges from global memory, four loads in
+// flight) and the runs united on the first pass — the loads and unions are
+// spread evenly over the CTA whatever the words look like, one union per
+// chain.  A full list falls back to `now(entry)`.  (k, 0) rows whose partner
+// row lies in another band: mc_axis_cross.
+struct AxisWord {
+    uint32_t cand, heads;
+};
+
+// candidate and chain-head bits of word w (row q of the band, word cw of the row) for axis offset o
+__device__ __forceinline__ AxisWord mc_axis_word(const KArgs &a, const uint32_t *P, const uint32_t *L,
+                                                 const uint32_t *U, const uint32_t *SB, int o, int w, int q, int cw) {
+    const int WPR = a.WPR;
+    const int dy = a.dy[o], k = a.dx[o] ? a.dx[o] : dy;
+    const uint32_t pw = P[w];
+    uint32_t cand, ltw;
+    if (dy == 0) {
+        const int wl = cw > 0 ? w - 1 : w + WPR - 1;   // word to the left (the seam wraps)
+        const uint32_t pt = (pw << k) | (P[wl] >> (32 - k));
+        ltw = (L[w] << k) | (L[wl] >> (32 - k));
+        // a run start in (c - k, c]; across the seam runs always differ
+        const uint32_t sb = SB[w], sbl = SB[wl];
+        uint32_t diff = cw == 0 ? (1u << k) - 1u : 0u;
+        for (int i = 0; i < k; ++i) diff |= (sb << i) | (i ? sbl >> (32 - i) : 0u);
+        cand = pw & pt & diff;
+    } else {
+        ltw = L[w - dy * WPR];
+        uint32_t chain = ~0u;
+        for (int i = 0; i < dy; ++i) chain &= U[w - i * WPR];
+        cand = pw & P[w - dy * WPR] & ~chain;
+    }
+    return {cand, cand & ~((cand << 1) & L[w] & ltw)};
+}
+
 template <class Now>
-__device__ __forceinline__ void mc_axis_list(const KArgs &a, const uint32_t *P, const uint32_t *L, const uint32_t *U,
-                                             const uint32_t *SB, const uint32_t *NB, const uint32_t *E, int r0,
-                                             int rows, int tid, int nthreads, uint32_t *list, uint32_t cap,
-                                             uint32_t *count, Now now) {
+__device__ __forceinline__ void mc_axis_heads(const KArgs &a, const uint32_t *P, const uint32_t *L, const uint32_t *U,
+                                              const uint32_t *SB, const uint32_t *NB, const uint32_t *E, int rows,
+                                              int tid, int nthreads, uint32_t *list, uint32_t cap, uint32_t *count,
+                                              Now now) {
     const int W = a.W, WPR = a.WPR;
     const int nw = rows * WPR;
     for (int o = 0; o < a.n_off; ++o) {
         if (!mc_axis_offset(a, o)) continue;
-        const int dy = a.dy[o], k = a.dx[o] ? a.dx[o] : dy;
-        const bool horiz = dy == 0;
-        for (int w = tid; w < nw; w += nthreads) {
+        const int dy = a.dy[o], dx = a.dx[o];
+        for (int w = dy * WPR + tid; w < nw; w += nthreads) {   // rows q < dy: partner row in another band (or none)
+            if (!P[w]) continue;
             const int q = divWPR(a, w), cw = w - q * WPR;
-            if (q < dy) continue;   // partner row in another band (or above the frame)
-            const uint32_t pw = P[w];
-            if (!pw) continue;
-            uint32_t cand, ltw;
-            if (horiz) {
-                const int wl = cw > 0 ? w - 1 : w + WPR - 1;   // word to the left (the seam wraps)
-                const uint32_t pt = (pw << k) | (P[wl] >> (32 - k));
-                ltw = (L[w] << k) | (L[wl] >> (32 - k));
-                // a run start in (c - k, c]; across the seam runs always differ
-                const uint32_t sb = SB[w], sbl = SB[wl];
-                uint32_t diff = cw == 0 ? (1u << k) - 1u : 0u;
-                for (int i = 0; i < k; ++i) diff |= (sb << i) | (i ? sbl >> (32 - i) : 0u);
-                cand = pw & pt & diff;
-            } else {
-                ltw = L[w - dy * WPR];
-                uint32_t chain = ~0u;
-                for (int i = 0; i < dy; ++i) chain &= U[w - i * WPR];
-                cand = pw & P[w - dy * WPR] & ~chain;
-            }
-            if (!cand) continue;
-            const uint32_t heads = cand & ~((cand << 1) & L[w] & ltw);   // bit 0 of a word is always a head
+            const AxisWord aw = mc_axis_word(a, P, L, U, SB, o, w, q, cw);
+            const uint32_t heads = aw.heads;
+            if (!heads) continue;
+            // heads whose two runs have different band-local roots (the words'
+            // run counts stay in registers across the heads)
             const int tqw = (q - dy) * WPR;
-            uint32_t live = 0;   // cells of chains whose runs have different roots
+            uint32_t live = 0;
             for (uint32_t m = heads; m; m &= m - 1) {
                 const int b = __ffs(m) - 1;
-                int tc = cw * 32 + b - (horiz ? k : 0);
+                int tc = cw * 32 + b - dx;
                 tc = tc < 0 ? tc + W : tc;
-                if (E[run_of(SB, NB, w, b)] == E[run_of(SB, NB, tqw + (tc >> 5), tc & 31)]) continue;
-                const uint32_t nxt = heads & ~lanemask_le(b);   // the chain: from b up to the next head
-                const uint32_t upto = nxt ? ((1u << (__ffs(nxt) - 1)) - 1u) : ~0u;
-                live |= cand & upto & ~((1u << b) - 1u);
+                if (E[run_of(SB, NB, w, b)] != E[run_of(SB, NB, tqw + (tc >> 5), tc & 31)]) live |= 1u << b;
             }
             if (!live) continue;
             uint32_t slot = atomicAdd(count, (uint32_t)__popc(live));
             for (uint32_t m = live; m; m &= m - 1, ++slot) {
-                const uint32_t e = (uint32_t)w | ((uint32_t)(__ffs(m) - 1) << 16) | ((uint32_t)o << 21);
-                if (slot < cap) list[slot] = e;
-                else now(e);
+                const int b = __ffs(m) - 1;
+                const uint32_t e = (uint32_t)w | ((uint32_t)b << 16) | ((uint32_t)o << 21);
+                // the chain: the candidates from b up to the next head of the word
+                const uint32_t nxt = aw.heads & ~lanemask_le(b);
+                const uint32_t upto = nxt ? ((1u << (__ffs(nxt) - 1)) - 1u) : ~0u;
+                const uint32_t cells = aw.cand & upto & ~((1u << b) - 1u);
+                if (slot < cap) {
+                    list[2 * slot] = e;
+                    list[2 * slot + 1] = cells;
+                } else {
+                    now(e, cells);
+                }
             }
         }
     }
 }
 
-// One listed cell of mc_axis_list: test the pair, `unite(x, y)` (run ids of the band) on a pass.
+// One listed chain (head entry e, cell bits `live`; its runs had different
+// roots): `unite(x, y)` (run ids of the band) if a cell of the chain passes.
 template <class Unite>
-__device__ __forceinline__ void mc_axis_cell(const KArgs &a, const uint32_t *SB, const uint32_t *NB, const float *fr,
-                                             int r0, uint32_t e, Unite unite) {
+__device__ __forceinline__ void mc_axis_chain(const KArgs &a, const uint32_t *P, const uint32_t *L, const uint32_t *U,
+                                              const uint32_t *SB, const uint32_t *NB, const float *fr, int r0,
+                                              uint32_t e, uint32_t live, Unite unite) {
     const int W = a.W, WPR = a.WPR, H = a.H;
     const int w = (int)(e & 0xffffu), b = (int)((e >> 16) & 31u), o = (int)(e >> 21);
     const int dy = a.dy[o], dx = a.dx[o];
     const int q = divWPR(a, w), cw = w - q * WPR;
-    const int r = r0 + q, tr = r - dy, c = cw * 32 + b;
-    int tc = c - dx;
-    tc = tc < 0 ? tc + W : tc;
-    const float vo = __ldg(fr + (size_t)r * W + c), vt = __ldg(fr + (size_t)tr * W + tc);
+    const int r = r0 + q, tr = r - dy;
     const float tco = __ldg(a.tables + 6 * H - 5 + o * H + tr);
-    if (pair_pass(vt, vo, tco, a.dmax2))
-        unite(run_of(SB, NB, w, b), run_of(SB, NB, (q - dy) * WPR + (tc >> 5), tc & 31));
+    const float *orow = fr + (size_t)r * W + cw * 32, *trow = fr + (size_t)tr * W;
+    for (uint32_t m = live; m;) {   // four cells per round: their loads overlap
+        float vo[4], vt[4];
+        bool on[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            on[j] = m != 0u;
+            vo[j] = vt[j] = 0.f;
+            if (m) {
+                const int bb = __ffs(m) - 1;
+                m &= m - 1;
+                int t = cw * 32 + bb - dx;
+                t = t < 0 ? t + W : t;
+                vo[j] = __ldg(orow + bb);
+                vt[j] = __ldg(trow + t);
+            }
+        }
+        bool pass = false;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) pass |= on[j] && pair_pass(vt[j], vo[j], tco, a.dmax2);
+        if (pass) {
+            int tc = cw * 32 + b - dx;
+            tc = tc < 0 ? tc + W : tc;
+            unite(run_of(SB, NB, w, b), run_of(SB, NB, (q - dy) * WPR + (tc >> 5), tc & 31));
+            return;
+        }
+    }
 }
 
 // (k, 0) pairs whose partner row lies in a band above (the first k rows of
-// the band): a lane per cell.  The other band's P / L / SB / NB planes are
-// read over DSMEM (final since step R; its U plane is not — the band may
-// already be listing cross-band edges in it — so every present pair is
-// tested: any passing pair may be united at any time, the components are
-// those of the graph of all passing edges).  Of consecutive passing pairs
-// whose own and partner cells are left-linked only the first is pushed.
-// push(has, x, y) is called by every lane (band-tagged run ids).
+// band bl): a lane per cell.  Like the cross-band up edges the work is shared
+// by the two bands of a boundary: band bl takes the upper half of the words,
+// band bl - 1 the lower half of the pairs whose partner row is its own (a
+// partner row further up — k > R — stays with band bl).  The other band's
+// P / L / SB / NB planes are read over DSMEM (final since step R; its U plane
+// is not — the band may already be listing cross-band edges in it — so every
+// present pair is tested: any passing pair may be united at any time, the
+// components are those of the graph of all passing edges).  Of consecutive
+// passing pairs whose own and partner cells are left-linked only the first is
+// pushed.  push(has, x, y) is called by every lane (band-tagged run ids).
 template <class Push>
-__device__ __forceinline__ void mc_axis_cross(const KArgs &a, const cg::cluster_group &cl, int kb, const uint32_t *P,
-                                              const uint32_t *L, const uint32_t *SB, const uint32_t *NB,
-                                              const float *fr, int r0, int rows, int lane, int warp, int nwarps,
+__device__ __forceinline__ void mc_axis_cross(const KArgs &a, const cg::cluster_group &cl, int kb, int bl,
+                                              const uint32_t *P, const uint32_t *L, const uint32_t *SB,
+                                              const uint32_t *NB, const float *fr, int lane, int warp, int nwarps,
                                               Push push) {
     const int W = a.W, WPR = a.WPR, R = a.R, H = a.H;
-    const uint32_t own_tag = (uint32_t)kb << a.SHN;
+    const int r0 = bl * R, rows = min(R, H - r0);   // the lower band
+    const bool lower = kb == bl;
+    const int whalf = WPR / 2;
+    auto plane = [&](const uint32_t *x, int band) { return band == kb ? x : cl.map_shared_rank(x, band); };
+    const uint32_t *Pl = plane(P, bl), *Ll = plane(L, bl), *SBl = plane(SB, bl), *NBl = plane(NB, bl);
+    const uint32_t low_tag = (uint32_t)bl << a.SHN;
     for (int o = 0; o < a.n_off; ++o) {
         if (!mc_axis_offset(a, o) || a.dy[o] == 0) continue;
         const int dy = a.dy[o];
         const int nq = min(dy, rows);
-        for (int wi = warp; wi < nq * WPR; wi += nwarps) {   // a warp per word (W % 32 == 0)
-            const int q = wi / WPR, cw = wi - q * WPR;
-            const int r = r0 + q, tr = r - dy;
-            if (tr < 0) continue;   // warp-uniform
-            const int kt = tr / R, tq = tr - kt * R;
-            const int w = q * WPR + cw, tw = tq * WPR + cw;
-            const uint32_t *Pp = cl.map_shared_rank(P, kt), *Lp = cl.map_shared_rank(L, kt);
-            const uint32_t both = P[w] & Pp[tw];
-            if (!both) continue;   // warp-uniform
-            const bool mine = (both >> lane) & 1u;
-            const int c = cw * 32 + lane;
-            bool pass = false;
-            if (mine)
-                pass = pair_pass(__ldg(fr + (size_t)tr * W + c), __ldg(fr + (size_t)r * W + c),
-                                 __ldg(a.tables + 6 * H - 5 + o * H + tr), a.dmax2);
-            const uint32_t m = __ballot_sync(kFull, pass);
-            const uint32_t dup = (m << 1) & L[w] & Lp[tw];   // the pair to the left passed and joins the same runs
-            const bool has = pass && !((dup >> lane) & 1u);
-            uint32_t x = 0, y = 0;
-            if (has) {
-                x = own_tag | run_of(SB, NB, w, lane);
-                y = ((uint32_t)kt << a.SHN) | run_of(cl.map_shared_rank(SB, kt), cl.map_shared_rank(NB, kt), tw, lane);
+        // a warp per word (W % 32 == 0), two words per round so that their
+        // DSMEM and global loads overlap
+        for (int wi0 = warp; wi0 < nq * WPR; wi0 += 2 * nwarps) {
+            int w[2], tw[2], kt[2];
+            uint32_t both[2];
+            float vo[2], vt[2], tco[2];
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const int wi = wi0 + j * nwarps;
+                both[j] = 0;
+                w[j] = tw[j] = kt[j] = 0;
+                vo[j] = vt[j] = tco[j] = 0.f;
+                if (wi >= nq * WPR) continue;   // warp-uniform
+                const int q = wi / WPR, cw = wi - q * WPR;
+                const int r = r0 + q, tr = r - dy;
+                if (tr < 0) continue;   // warp-uniform
+                kt[j] = tr / R;
+                // whose word is it?  shared pairs (partner row in band bl - 1) by halves
+                const bool shared = kt[j] == bl - 1;
+                if (lower ? (shared && cw < whalf) : !(shared && cw < whalf)) continue;
+                w[j] = q * WPR + cw;
+                tw[j] = (tr - kt[j] * R) * WPR + cw;
+                both[j] = Pl[w[j]] & plane(P, kt[j])[tw[j]];
+                if ((both[j] >> lane) & 1u) {
+                    const int c = cw * 32 + lane;
+                    vt[j] = __ldg(fr + (size_t)tr * W + c);
+                    vo[j] = __ldg(fr + (size_t)r * W + c);
+                    tco[j] = __ldg(a.tables + 6 * H - 5 + o * H + tr);
+                }
             }
-            push(has, x, y);
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                if (!both[j]) continue;   // warp-uniform
+                const bool pass = ((both[j] >> lane) & 1u) && pair_pass(vt[j], vo[j], tco[j], a.dmax2);
+                const uint32_t m = __ballot_sync(kFull, pass);
+                if (!m) continue;
+                // the pair to the left passed and joins the same runs
+                const uint32_t dup = (m << 1) & Ll[w[j]] & plane(L, kt[j])[tw[j]];
+                const bool has = pass && !((dup >> lane) & 1u);
+                uint32_t x = 0, y = 0;
+                if (has) {
+                    x = low_tag | run_of(SBl, NBl, w[j], lane);
+                    y = ((uint32_t)kt[j] << a.SHN) | run_of(plane(SB, kt[j]), plane(NB, kt[j]), tw[j], lane);
+                }
+                push(has, x, y);
+            }
         }
     }
 }
