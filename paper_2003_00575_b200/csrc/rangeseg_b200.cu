@@ -357,13 +357,18 @@ int launch_cluster(Kern kern, const KArgs &k, int clusters, int threads, size_t 
     lc.blockDim = dim3((unsigned)threads, 1, 1);
     lc.dynamicSmemBytes = smem;
     lc.stream = stream;
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = (unsigned)k.C;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
     lc.attrs = at;
     lc.numAttrs = 1;
+    // the hardware may place the CTAs of a cluster where there is room instead
+    // of spreading them (measured: config 1 163.1 vs 164.1 us, config 2 196.2 vs 197.3)
+    at[1].id = cudaLaunchAttributeClusterSchedulingPolicyPreference;
+    at[1].val.clusterSchedulingPolicyPreference = cudaClusterSchedulingPolicyLoadBalancing;
+    lc.numAttrs = 2;
     return cuda_check(cudaLaunchKernelEx(&lc, kern, k), what);
 }
 

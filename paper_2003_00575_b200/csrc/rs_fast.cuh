@@ -51,6 +51,9 @@ namespace rs {
 #ifndef RS_UDYN_GRAB
 #define RS_UDYN_GRAB 2   // dynamic local unions: contiguous edges per lane and grab (measured 1, 2, 4, 8)
 #endif
+#ifndef RS_PF_L2
+#define RS_PF_L2 0   // step A: L2 prefetch this many rows beyond the register prefetch (0 = off)
+#endif
 #ifndef RS_STRIP_SETS
 #define RS_STRIP_SETS 4   // step A register sets: 4 = two-row prefetch, 3 = one-row prefetch
 #endif
@@ -229,6 +232,12 @@ struct BitsStrip {
                                          float (&vn)[4]) const {
         if (!ROW0 && !RING) {   // prefetch row r + RS_STRIP_SETS - 2
             ldp(np, vn, r + RS_STRIP_SETS - 2 < rend);
+#if RS_PF_L2 > 0
+            // and pull the row RS_PF_L2 further down into L2 (the chunk's four
+            // 128-byte lines, eight lanes each; the frame's rows only)
+            if (r + RS_STRIP_SETS - 2 + RS_PF_L2 < a.H)
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(np + RS_PF_L2 * rowf - lane + (lane & 3) * 32));
+#endif
             np += rowf;
         }
         const float4 c = *reinterpret_cast<const float4 *>(rowc + (r - rstart) * 8);
@@ -827,65 +836,79 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
             }
         };
         flatten();
-        if (MC && tid == 0) n_edges = 0;
+        if (MC && tid == 0) n_edges = ucur = 0;
         __syncthreads();
         RS_MARK(5);
-        if (MC && a.n_off > 0 && !a.planes) {
-            // ---- Map Connections of the skip offsets (0, k) / (k, 0) inside the
-            // band (rs_mc.cuh: mc_axis_heads / mc_axis_chain), while nothing
-            // outside the CTA touches its forest: chains of candidate pairs whose
-            // runs have different local roots are listed (the size array is
-            // the buffer), then tested and united by all threads, and the
-            // forest is flattened again.  Rows whose partner row lies in another band
-            // are handled with the cross-band edges (step X).
+        if (MC && a.n_off > 0 && !a.planes && (W & 31) == 0) {
+            // ---- Map Connections inside the band (rs_mc.cuh: mc_axis_heads /
+            // mc_chain_issue / mc_chain_finish), while nothing outside the CTA
+            // touches its forest: chains of candidate pairs whose runs have
+            // different local roots are listed (the size array is the
+            // buffer), then tested and united by all threads, and the forest
+            // is flattened again.  One round for the skip offsets (0, k) /
+            // (k, 0) together (few candidates: only where the straight chain
+            // of links is broken), one round for every other offset (every
+            // present pair is a candidate; the re-flattened forest of the
+            // earlier rounds rules most of them out).  Rows whose partner row
+            // lies in another band are handled with the cross-band edges
+            // (step X).
             const uint32_t lcap = (uint32_t)a.NC / 2u;   // two words per chain
+            auto ul = [&](uint32_t x, uint32_t y) { uf.unite_local(band | x, band | y); };
             auto chain = [&](uint32_t e, uint32_t cells) {
-                mc_axis_chain(a, P, L, U, SB, NB, fr, r0, e, cells,
-                              [&](uint32_t x, uint32_t y) { uf.unite_local(band | x, band | y); });
+                mc_chain_finish(a, SB, NB, fr, r0, e, cells, mc_chain_issue(a, fr, r0, e, cells), ul);
             };
-            mc_axis_heads(a, P, L, U, SB, NB, E, rows, tid, kFastThreads, SZ, lcap, &n_edges, chain);
-            __syncthreads();
-            const uint32_t nl = min(n_edges, lcap);
-            const bool any = nl != 0u;   // block-uniform
-            for (uint32_t i = tid; i < nl; i += kFastThreads) {
-                const uint32_t e = SZ[2 * i], cells = SZ[2 * i + 1];
-                SZ[2 * i] = SZ[2 * i + 1] = 0;
-                chain(e, cells);
-            }
-            RS_MARK(21);
-            if (any) {
-                // flatten again, in two steps: the roots of the first flatten
-                // (LR bits; every other run points at one of them) find their
-                // new root, then every run takes one hop
+            uint32_t *cnt = &n_edges, *cnt_next = &ucur;   // list counters of this / the next round (both zero)
+            for (int o0 = 0; o0 < a.n_off;) {
+                int o1 = o0 + 1;
+                if (mc_axis_offset(a, o0))
+                    while (o1 < a.n_off && mc_axis_offset(a, o1)) ++o1;   // consecutive skip offsets share a round
+                mc_axis_heads(a, o0, o1, P, L, U, SB, NB, E, rows, tid, kFastThreads, SZ, lcap, cnt, chain);
                 __syncthreads();
-                // (pointer jumping: every such root repeats E[r] = E[E[r]] while
-                // the others do the same, so a chain of hooks of any depth —
-                // skips merge runs along a row one after the other — takes a
-                // logarithmic number of steps)
-                for (uint32_t w = warp; w < (n_runs + 31) / 32; w += kFastWarps) {
-                    const uint32_t id = w * 32 + lane;
-                    if (!((LR[w] >> lane) & 1u)) continue;
-                    volatile uint32_t *V = E;
-                    while (true) {
-                        const uint32_t p = V[id];
-                        const uint32_t gp = V[p & maskN];
-                        if (gp == p) break;
-                        V[id] = gp;
-                    }
+                const uint32_t nl = min(*cnt, lcap);   // block-uniform
+                for (uint32_t i = tid; i < nl; i += kFastThreads) {
+                    const uint32_t e = SZ[2 * i], cells = SZ[2 * i + 1];
+                    SZ[2 * i] = SZ[2 * i + 1] = 0;
+                    chain(e, cells);
                 }
                 __syncthreads();
-                for (uint32_t base = warp * 32; base < n_runs; base += kFastThreads) {
-                    const uint32_t id = base + lane;
-                    bool lr = false;
-                    if (id < n_runs) {
-                        const uint32_t r = E[E[id] & maskN];
-                        E[id] = r;
-                        lr = r == (band | id);
+                // every thread has read this round's counter: zero it for the round
+                // after the next (nobody touches it during the next round)
+                if (tid == 0) *cnt = 0;
+                uint32_t *t = cnt; cnt = cnt_next; cnt_next = t;
+                if (nl) {
+                    // flatten again, in two steps: the roots of the last flatten
+                    // (LR bits; every other run points at one of them) find
+                    // their new root by pointer jumping (every such root repeats
+                    // E[r] = E[E[r]] while the others do the same, so a chain of
+                    // hooks of any depth — skips merge runs along a row one
+                    // after the other — takes a logarithmic number of steps),
+                    // then every run takes one hop
+                    for (uint32_t w = warp; w < (n_runs + 31) / 32; w += kFastWarps) {
+                        const uint32_t id = w * 32 + lane;
+                        if (!((LR[w] >> lane) & 1u)) continue;
+                        volatile uint32_t *V = E;
+                        while (true) {
+                            const uint32_t p = V[id];
+                            const uint32_t gp = V[p & maskN];
+                            if (gp == p) break;
+                            V[id] = gp;
+                        }
                     }
-                    const uint32_t m = __ballot_sync(kFull, lr);
-                    if (lane == 0) LR[base >> 5] = m;
+                    __syncthreads();
+                    for (uint32_t base = warp * 32; base < n_runs; base += kFastThreads) {
+                        const uint32_t id = base + lane;
+                        bool lr = false;
+                        if (id < n_runs) {
+                            const uint32_t r = E[E[id] & maskN];
+                            E[id] = r;
+                            lr = r == (band | id);
+                        }
+                        const uint32_t m = __ballot_sync(kFull, lr);
+                        if (lane == 0) LR[base >> 5] = m;
+                    }
+                    __syncthreads();
                 }
-                __syncthreads();
+                o0 = o1;
             }
             RS_MARK(22);
         }
@@ -943,16 +966,11 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
     }
 
     RS_MARK(7);
-    // Map Connections: the skip offsets (0, k) / (k, 0) were united inside the
-    // band before barrier #1 and are finished with the cross-band edges below;
-    // step M is only needed for other offsets (and for the parity export)
-    const bool axis = MC && a.n_off > 0 && !a.planes;
-    bool mstep = MC && a.n_off > 0;
-    if (axis) {
-        bool all_axis = true;
-        for (int o = 0; o < a.n_off; ++o) all_axis &= mc_axis_offset(a, o);
-        mstep = !all_axis;
-    }
+    // Map Connections were united inside the band before barrier #1 and are
+    // finished with the cross-band edges below; step M is only needed for the
+    // parity export and for widths that are not whole words
+    const bool inband = MC && a.n_off > 0 && !a.planes && (W & 31) == 0;
+    const bool mstep = MC && a.n_off > 0 && !inband;
     // ---- X. cross-band unions over DSMEM -----------------------------------
     // Boundary edges are listed first (rows 1.. of the U plane are free now and
     // serve as the buffer), then united by all threads in parallel.  The up
@@ -1005,10 +1023,10 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
         const int whalf = WPR / 2;
         if (r0 > 0) boundary(k, whalf, WPR);
         if (k + 1 < a.C) boundary(k + 1, 0, whalf);
-        // (k, 0) Map Connection pairs whose partner row lies in a band above:
-        // a lane per cell, passing pairs join the cross-band edge list; shared
-        // by the two bands of a boundary like the up edges
-        if (axis) {
+        // Map Connection pairs whose partner row lies in a band above: a lane
+        // per cell, passing pairs join the cross-band edge list; shared by the
+        // two bands of a boundary like the up edges
+        if (inband) {
             if (r0 > 0) mc_axis_cross(a, cl, k, k, P, L, SB, NB, fr, lane, warp, kFastWarps, xpush);
             if (k + 1 < a.C) mc_axis_cross(a, cl, k, k + 1, P, L, SB, NB, fr, lane, warp, kFastWarps, xpush);
         }
@@ -1042,7 +1060,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
             return ((uint32_t)kt << a.SHN) | run_of(SBt, NBt, tw, tb);
         };
         if (!exp)
-            mc_runs(a, cl, k, P, L, SB, NB, fr, r0, rows, n_runs, tid, kFastThreads, ML, mcap, &ucur, axis,
+            mc_runs(a, cl, k, P, L, SB, NB, fr, r0, rows, n_runs, tid, kFastThreads, ML, mcap, &ucur,
                     [&](int kt, uint32_t id) { return kt == k ? E[id] : *cl.map_shared_rank(E + id, kt); },
                     [&](int kt, uint32_t id) { return uf.find_nc(((uint32_t)kt << a.SHN) | id); },
                     [&](uint32_t x, uint32_t y) { uf.unite_roots(x, y); });

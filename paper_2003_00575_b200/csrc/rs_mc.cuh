@@ -171,7 +171,7 @@ __device__ __forceinline__ bool mc_axis_offset(const KArgs &a, int o) {
 // are compared once, at its head (bit 0 of a word is always a head), and the
 // heads whose roots differ are LISTED (entry = word | bit << 16 | offset <<
 // 21, and the chain's cell bits: two words, `cap` entries).  The caller then
-// gives every listed head to a thread (mc_axis_chain):
+// gives every listed head to a thread (mc_chain_issue / mc_chain_finish):
 // the chain's cells are tested (ranges from global memory, four loads in
 // flight) and the runs united on the first pass — the loads and unions are
 // spread evenly over the CTA whatever the words look like, one union per
@@ -187,7 +187,7 @@ __device__ __forceinline__ AxisWord mc_axis_word(const KArgs &a, const uint32_t 
     const int WPR = a.WPR;
     const int dy = a.dy[o], k = a.dx[o] ? a.dx[o] : dy;
     const uint32_t pw = P[w];
-    uint32_t cand, ltw;
+    uint32_t cand = 0, ltw = 0;
     if (dy == 0) {
         const int wl = cw > 0 ? w - 1 : w + WPR - 1;   // word to the left (the seam wraps)
         const uint32_t pt = (pw << k) | (P[wl] >> (32 - k));
@@ -197,7 +197,7 @@ __device__ __forceinline__ AxisWord mc_axis_word(const KArgs &a, const uint32_t 
         uint32_t diff = cw == 0 ? (1u << k) - 1u : 0u;
         for (int i = 0; i < k; ++i) diff |= (sb << i) | (i ? sbl >> (32 - i) : 0u);
         cand = pw & pt & diff;
-    } else {
+    } else if (a.dx[o] == 0) {
         ltw = L[w - dy * WPR];
         uint32_t chain = ~0u;
         for (int i = 0; i < dy; ++i) chain &= U[w - i * WPR];
@@ -206,20 +206,41 @@ __device__ __forceinline__ AxisWord mc_axis_word(const KArgs &a, const uint32_t 
     return {cand, cand & ~((cand << 1) & L[w] & ltw)};
 }
 
+// the same for any other offset (no straight chain of links to rule pairs
+// out): every present pair is a candidate; the partner row's bits are brought
+// under the own columns with a funnel shift of two of its words
+__device__ __forceinline__ AxisWord mc_any_word(const KArgs &a, const uint32_t *P, const uint32_t *L, int o, int w,
+                                                int q, int cw) {
+    const int WPR = a.WPR;
+    int t0 = (cw * 32 - a.dx[o]) % a.W;   // partner column of the word's bit 0
+    t0 = t0 < 0 ? t0 + a.W : t0;
+    const int tqw = (q - a.dy[o]) * WPR;
+    const uint32_t cand = P[w] & row_bits(P + tqw, t0, a.W, WPR, 0, true);
+    const uint32_t ltw = row_bits(L + tqw, t0, a.W, WPR, 0, true);
+    return {cand, cand & ~((cand << 1) & L[w] & ltw)};
+}
+
+// partner column of column c for offset dx (|dx| < W)
+__device__ __forceinline__ int mc_partner_col(int c, int dx, int W) {
+    const int t = c - dx;
+    return t < 0 ? t + W : (t >= W ? t - W : t);
+}
+
+// offsets [o0, o1) of the pattern
 template <class Now>
-__device__ __forceinline__ void mc_axis_heads(const KArgs &a, const uint32_t *P, const uint32_t *L, const uint32_t *U,
-                                              const uint32_t *SB, const uint32_t *NB, const uint32_t *E, int rows,
-                                              int tid, int nthreads, uint32_t *list, uint32_t cap, uint32_t *count,
-                                              Now now) {
+__device__ __forceinline__ void mc_axis_heads(const KArgs &a, int o0, int o1, const uint32_t *P, const uint32_t *L,
+                                              const uint32_t *U, const uint32_t *SB, const uint32_t *NB,
+                                              const uint32_t *E, int rows, int tid, int nthreads, uint32_t *list,
+                                              uint32_t cap, uint32_t *count, Now now) {
     const int W = a.W, WPR = a.WPR;
     const int nw = rows * WPR;
-    for (int o = 0; o < a.n_off; ++o) {
-        if (!mc_axis_offset(a, o)) continue;
+    for (int o = o0; o < o1; ++o) {
         const int dy = a.dy[o], dx = a.dx[o];
+        const bool axis = mc_axis_offset(a, o);
         for (int w = dy * WPR + tid; w < nw; w += nthreads) {   // rows q < dy: partner row in another band (or none)
             if (!P[w]) continue;
             const int q = divWPR(a, w), cw = w - q * WPR;
-            const AxisWord aw = mc_axis_word(a, P, L, U, SB, o, w, q, cw);
+            const AxisWord aw = axis ? mc_axis_word(a, P, L, U, SB, o, w, q, cw) : mc_any_word(a, P, L, o, w, q, cw);
             const uint32_t heads = aw.heads;
             if (!heads) continue;
             // heads whose two runs have different band-local roots (the words'
@@ -228,8 +249,7 @@ __device__ __forceinline__ void mc_axis_heads(const KArgs &a, const uint32_t *P,
             uint32_t live = 0;
             for (uint32_t m = heads; m; m &= m - 1) {
                 const int b = __ffs(m) - 1;
-                int tc = cw * 32 + b - dx;
-                tc = tc < 0 ? tc + W : tc;
+                const int tc = mc_partner_col(cw * 32 + b, dx, W);
                 if (E[run_of(SB, NB, w, b)] != E[run_of(SB, NB, tqw + (tc >> 5), tc & 31)]) live |= 1u << b;
             }
             if (!live) continue;
@@ -253,57 +273,90 @@ __device__ __forceinline__ void mc_axis_heads(const KArgs &a, const uint32_t *P,
 }
 
 // One listed chain (head entry e, cell bits `live`; its runs had different
-// roots): `unite(x, y)` (run ids of the band) if a cell of the chain passes.
-template <class Unite>
-__device__ __forceinline__ void mc_axis_chain(const KArgs &a, const uint32_t *P, const uint32_t *L, const uint32_t *U,
-                                              const uint32_t *SB, const uint32_t *NB, const float *fr, int r0,
-                                              uint32_t e, uint32_t live, Unite unite) {
+// roots), in two halves so that a thread can keep several chains' loads in
+// flight: mc_chain_issue loads the ranges of the chain's first two cells,
+// mc_chain_finish tests them, goes on through the rest of the chain (four
+// loads in flight) while none passes, and calls `unite(x, y)` (run ids of the
+// band) on the first pass.
+struct ChainLoads {
+    float vo[2], vt[2], tco;
+};
+
+__device__ __forceinline__ ChainLoads mc_chain_issue(const KArgs &a, const float *fr, int r0, uint32_t e,
+                                                     uint32_t live) {
     const int W = a.W, WPR = a.WPR, H = a.H;
-    const int w = (int)(e & 0xffffu), b = (int)((e >> 16) & 31u), o = (int)(e >> 21);
+    const int w = (int)(e & 0xffffu), o = (int)(e >> 21);
     const int dy = a.dy[o], dx = a.dx[o];
     const int q = divWPR(a, w), cw = w - q * WPR;
     const int r = r0 + q, tr = r - dy;
-    const float tco = __ldg(a.tables + 6 * H - 5 + o * H + tr);
+    ChainLoads c;
+    c.tco = __ldg(a.tables + 6 * H - 5 + o * H + tr);
     const float *orow = fr + (size_t)r * W + cw * 32, *trow = fr + (size_t)tr * W;
-    for (uint32_t m = live; m;) {   // four cells per round: their loads overlap
-        float vo[4], vt[4];
-        bool on[4];
+    uint32_t m = live;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            on[j] = m != 0u;
-            vo[j] = vt[j] = 0.f;
-            if (m) {
-                const int bb = __ffs(m) - 1;
-                m &= m - 1;
-                int t = cw * 32 + bb - dx;
-                t = t < 0 ? t + W : t;
-                vo[j] = __ldg(orow + bb);
-                vt[j] = __ldg(trow + t);
+    for (int j = 0; j < 2; ++j) {
+        c.vo[j] = c.vt[j] = 0.f;
+        if (m) {
+            const int bb = __ffs(m) - 1;
+            m &= m - 1;
+            c.vo[j] = __ldg(orow + bb);
+            c.vt[j] = __ldg(trow + mc_partner_col(cw * 32 + bb, dx, W));
+        }
+    }
+    return c;
+}
+
+template <class Unite>
+__device__ __forceinline__ void mc_chain_finish(const KArgs &a, const uint32_t *SB, const uint32_t *NB,
+                                                const float *fr, int r0, uint32_t e, uint32_t live,
+                                                const ChainLoads &c, Unite unite) {
+    const int W = a.W, WPR = a.WPR;
+    const int w = (int)(e & 0xffffu), b = (int)((e >> 16) & 31u), o = (int)(e >> 21);
+    const int dy = a.dy[o], dx = a.dx[o];
+    const int q = divWPR(a, w), cw = w - q * WPR;
+    uint32_t m = live & (live - 1);   // the cells after the first
+    const bool two = m != 0u;
+    m &= m - 1;
+    bool pass = pair_pass(c.vt[0], c.vo[0], c.tco, a.dmax2) || (two && pair_pass(c.vt[1], c.vo[1], c.tco, a.dmax2));
+    if (!pass && m) {
+        const int r = r0 + q, tr = r - dy;
+        const float *orow = fr + (size_t)r * W + cw * 32, *trow = fr + (size_t)tr * W;
+        while (m && !pass) {   // four cells per round: their loads overlap
+            float vo[4], vt[4];
+            bool on[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                on[j] = m != 0u;
+                vo[j] = vt[j] = 0.f;
+                if (m) {
+                    const int bb = __ffs(m) - 1;
+                    m &= m - 1;
+                    vo[j] = __ldg(orow + bb);
+                    vt[j] = __ldg(trow + mc_partner_col(cw * 32 + bb, dx, W));
+                }
             }
-        }
-        bool pass = false;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) pass |= on[j] && pair_pass(vt[j], vo[j], tco, a.dmax2);
-        if (pass) {
-            int tc = cw * 32 + b - dx;
-            tc = tc < 0 ? tc + W : tc;
-            unite(run_of(SB, NB, w, b), run_of(SB, NB, (q - dy) * WPR + (tc >> 5), tc & 31));
-            return;
+            for (int j = 0; j < 4; ++j) pass |= on[j] && pair_pass(vt[j], vo[j], c.tco, a.dmax2);
         }
+    }
+    if (pass) {
+        const int tc = mc_partner_col(cw * 32 + b, dx, W);
+        unite(run_of(SB, NB, w, b), run_of(SB, NB, (q - dy) * WPR + (tc >> 5), tc & 31));
     }
 }
 
-// (k, 0) pairs whose partner row lies in a band above (the first k rows of
-// band bl): a lane per cell.  Like the cross-band up edges the work is shared
-// by the two bands of a boundary: band bl takes the upper half of the words,
-// band bl - 1 the lower half of the pairs whose partner row is its own (a
-// partner row further up — k > R — stays with band bl).  The other band's
-// P / L / SB / NB planes are read over DSMEM (final since step R; its U plane
-// is not — the band may already be listing cross-band edges in it — so every
-// present pair is tested: any passing pair may be united at any time, the
-// components are those of the graph of all passing edges).  Of consecutive
-// passing pairs whose own and partner cells are left-linked only the first is
-// pushed.  push(has, x, y) is called by every lane (band-tagged run ids).
+// Pairs of offsets with dy > 0 whose partner row lies in a band above (the
+// first dy rows of band bl): a lane per cell.  Like the cross-band up edges
+// the work is shared by the two bands of a boundary: band bl takes the upper
+// half of the words, band bl - 1 the lower half of the pairs whose partner
+// row is its own (a partner row further up — dy > R — stays with band bl).
+// The other band's P / L / SB / NB planes are read over DSMEM (final since
+// step R; its U plane is not — the band may already be listing cross-band
+// edges in it — so every present pair is tested: any passing pair may be
+// united at any time, the components are those of the graph of all passing
+// edges).  Of consecutive passing pairs whose own and partner cells are
+// left-linked only the first is pushed.  push(has, x, y) is called by every
+// lane (band-tagged run ids).
 template <class Push>
 __device__ __forceinline__ void mc_axis_cross(const KArgs &a, const cg::cluster_group &cl, int kb, int bl,
                                               const uint32_t *P, const uint32_t *L, const uint32_t *SB,
@@ -317,20 +370,20 @@ __device__ __forceinline__ void mc_axis_cross(const KArgs &a, const cg::cluster_
     const uint32_t *Pl = plane(P, bl), *Ll = plane(L, bl), *SBl = plane(SB, bl), *NBl = plane(NB, bl);
     const uint32_t low_tag = (uint32_t)bl << a.SHN;
     for (int o = 0; o < a.n_off; ++o) {
-        if (!mc_axis_offset(a, o) || a.dy[o] == 0) continue;
-        const int dy = a.dy[o];
+        const int dy = a.dy[o], dx = a.dx[o];
+        if (dy == 0) continue;
         const int nq = min(dy, rows);
         // a warp per word (W % 32 == 0), two words per round so that their
         // DSMEM and global loads overlap
         for (int wi0 = warp; wi0 < nq * WPR; wi0 += 2 * nwarps) {
-            int w[2], tw[2], kt[2];
-            uint32_t both[2];
+            int w[2], twr[2], kt[2], tc[2];
+            uint32_t both[2], ltw[2];
             float vo[2], vt[2], tco[2];
 #pragma unroll
             for (int j = 0; j < 2; ++j) {
                 const int wi = wi0 + j * nwarps;
-                both[j] = 0;
-                w[j] = tw[j] = kt[j] = 0;
+                both[j] = ltw[j] = 0;
+                w[j] = twr[j] = kt[j] = tc[j] = 0;
                 vo[j] = vt[j] = tco[j] = 0.f;
                 if (wi >= nq * WPR) continue;   // warp-uniform
                 const int q = wi / WPR, cw = wi - q * WPR;
@@ -341,12 +394,15 @@ __device__ __forceinline__ void mc_axis_cross(const KArgs &a, const cg::cluster_
                 const bool shared = kt[j] == bl - 1;
                 if (lower ? (shared && cw < whalf) : !(shared && cw < whalf)) continue;
                 w[j] = q * WPR + cw;
-                tw[j] = (tr - kt[j] * R) * WPR + cw;
-                both[j] = Pl[w[j]] & plane(P, kt[j])[tw[j]];
+                twr[j] = (tr - kt[j] * R) * WPR;   // first word of the partner row in its band
+                const int t0 = mc_partner_col(cw * 32, dx, W);
+                both[j] = Pl[w[j]] & row_bits(plane(P, kt[j]) + twr[j], t0, W, WPR, 0, true);
+                if (!both[j]) continue;   // warp-uniform
+                ltw[j] = row_bits(plane(L, kt[j]) + twr[j], t0, W, WPR, 0, true);
+                tc[j] = mc_partner_col(cw * 32 + lane, dx, W);
                 if ((both[j] >> lane) & 1u) {
-                    const int c = cw * 32 + lane;
-                    vt[j] = __ldg(fr + (size_t)tr * W + c);
-                    vo[j] = __ldg(fr + (size_t)r * W + c);
+                    vt[j] = __ldg(fr + (size_t)tr * W + tc[j]);
+                    vo[j] = __ldg(fr + (size_t)r * W + cw * 32 + lane);
                     tco[j] = __ldg(a.tables + 6 * H - 5 + o * H + tr);
                 }
             }
@@ -357,12 +413,13 @@ __device__ __forceinline__ void mc_axis_cross(const KArgs &a, const cg::cluster_
                 const uint32_t m = __ballot_sync(kFull, pass);
                 if (!m) continue;
                 // the pair to the left passed and joins the same runs
-                const uint32_t dup = (m << 1) & Ll[w[j]] & plane(L, kt[j])[tw[j]];
+                const uint32_t dup = (m << 1) & Ll[w[j]] & ltw[j];
                 const bool has = pass && !((dup >> lane) & 1u);
                 uint32_t x = 0, y = 0;
                 if (has) {
                     x = low_tag | run_of(SBl, NBl, w[j], lane);
-                    y = ((uint32_t)kt[j] << a.SHN) | run_of(plane(SB, kt[j]), plane(NB, kt[j]), tw[j], lane);
+                    y = ((uint32_t)kt[j] << a.SHN) |
+                        run_of(plane(SB, kt[j]), plane(NB, kt[j]), twr[j] + (tc[j] >> 5), tc[j] & 31);
                 }
                 push(has, x, y);
             }
@@ -396,7 +453,7 @@ template <class Root, class Live, class Unite>
 __device__ __forceinline__ void mc_runs(const KArgs &a, const cg::cluster_group &cl, int k, const uint32_t *P,
                                         const uint32_t *L, const uint32_t *SB, const uint32_t *NB, const float *fr,
                                         int r0, int rows, uint32_t n_runs, int tid, int nthreads, uint32_t *list,
-                                        uint32_t cap, uint32_t *count, bool axis_done, Root root, Live live,
+                                        uint32_t cap, uint32_t *count, Root root, Live live,
                                         Unite unite) {
     const int H = a.H, W = a.W, R = a.R, WPR = a.WPR;
     const float thr = a.dmax2;
@@ -442,8 +499,6 @@ __device__ __forceinline__ void mc_runs(const KArgs &a, const cg::cluster_group 
         // axis offsets done by mc_axis: none left for (0, k); for (k, 0) only
         // the runs of rows q < dy (run ids follow cell order: ids below the
         // first run of row dy)
-        // axis offsets were done by mc_axis (every row, cross-band rows included)
-        if (axis_done && mc_axis_offset(a, o)) continue;   // uniform: skips the round's barriers too
         const uint32_t n_own = n_runs;
         if (tid == 0) *count = 0;
         __syncthreads();
