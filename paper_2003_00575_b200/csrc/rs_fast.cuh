@@ -1026,13 +1026,33 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
         // Map Connection pairs whose partner row lies in a band above: a lane
         // per cell, passing pairs join the cross-band edge list; shared by the
         // two bands of a boundary like the up edges
+        // The first such offset shares the list with the up edges; after that
+        // the list is united and reused per offset, and the unions so far
+        // rule out most of the later offsets' pairs (roots compared per chain).
+        auto flush = [&]() {
+            __syncthreads();
+            const uint32_t nx = min(n_xedges, xcap);
+            for (uint32_t e = tid; e < nx; e += kFastThreads) uf.unite(XL[2 * e], XL[2 * e + 1]);
+        };
         if (inband) {
-            if (r0 > 0) mc_axis_cross(a, cl, k, k, P, L, SB, NB, fr, lane, warp, kFastWarps, xpush);
-            if (k + 1 < a.C) mc_axis_cross(a, cl, k, k + 1, P, L, SB, NB, fr, lane, warp, kFastWarps, xpush);
+            auto xroot = [&](uint32_t e) { return uf.find_nc(uf.ld(e)); };
+            bool first = true;
+            for (int o = 0; o < a.n_off; ++o) {
+                if (a.dy[o] == 0) continue;
+                if (!first) {
+                    flush();
+                    __syncthreads();
+                    if (tid == 0) n_xedges = 0;
+                    __syncthreads();
+                }
+                if (r0 > 0)
+                    mc_axis_cross(a, cl, k, k, o, P, L, SB, NB, fr, lane, warp, kFastWarps, !first, xroot, xpush);
+                if (k + 1 < a.C)
+                    mc_axis_cross(a, cl, k, k + 1, o, P, L, SB, NB, fr, lane, warp, kFastWarps, !first, xroot, xpush);
+                first = false;
+            }
         }
-        __syncthreads();
-        const uint32_t nx = min(n_xedges, xcap);
-        for (uint32_t e = tid; e < nx; e += kFastThreads) uf.unite(XL[2 * e], XL[2 * e + 1]);
+        flush();
     }
     RS_STOP(5);
     RS_MARK(8);

@@ -357,11 +357,11 @@ __device__ __forceinline__ void mc_chain_finish(const KArgs &a, const uint32_t *
 // edges).  Of consecutive passing pairs whose own and partner cells are
 // left-linked only the first is pushed.  push(has, x, y) is called by every
 // lane (band-tagged run ids).
-template <class Push>
-__device__ __forceinline__ void mc_axis_cross(const KArgs &a, const cg::cluster_group &cl, int kb, int bl,
+template <class Root, class Push>
+__device__ __forceinline__ void mc_axis_cross(const KArgs &a, const cg::cluster_group &cl, int kb, int bl, int o,
                                               const uint32_t *P, const uint32_t *L, const uint32_t *SB,
                                               const uint32_t *NB, const float *fr, int lane, int warp, int nwarps,
-                                              Push push) {
+                                              bool filter, Root root, Push push) {
     const int W = a.W, WPR = a.WPR, R = a.R, H = a.H;
     const int r0 = bl * R, rows = min(R, H - r0);   // the lower band
     const bool lower = kb == bl;
@@ -369,9 +369,9 @@ __device__ __forceinline__ void mc_axis_cross(const KArgs &a, const cg::cluster_
     auto plane = [&](const uint32_t *x, int band) { return band == kb ? x : cl.map_shared_rank(x, band); };
     const uint32_t *Pl = plane(P, bl), *Ll = plane(L, bl), *SBl = plane(SB, bl), *NBl = plane(NB, bl);
     const uint32_t low_tag = (uint32_t)bl << a.SHN;
-    for (int o = 0; o < a.n_off; ++o) {
+    {
         const int dy = a.dy[o], dx = a.dx[o];
-        if (dy == 0) continue;
+        if (dy == 0) return;
         const int nq = min(dy, rows);
         // a warp per word (W % 32 == 0), two words per round so that their
         // DSMEM and global loads overlap
@@ -379,10 +379,12 @@ __device__ __forceinline__ void mc_axis_cross(const KArgs &a, const cg::cluster_
             int w[2], twr[2], kt[2], tc[2];
             uint32_t both[2], ltw[2];
             float vo[2], vt[2], tco[2];
+            bool diff[2];
 #pragma unroll
             for (int j = 0; j < 2; ++j) {
                 const int wi = wi0 + j * nwarps;
                 both[j] = ltw[j] = 0;
+                diff[j] = false;
                 w[j] = twr[j] = kt[j] = tc[j] = 0;
                 vo[j] = vt[j] = tco[j] = 0.f;
                 if (wi >= nq * WPR) continue;   // warp-uniform
@@ -400,7 +402,25 @@ __device__ __forceinline__ void mc_axis_cross(const KArgs &a, const cg::cluster_
                 if (!both[j]) continue;   // warp-uniform
                 ltw[j] = row_bits(plane(L, kt[j]) + twr[j], t0, W, WPR, 0, true);
                 tc[j] = mc_partner_col(cw * 32 + lane, dx, W);
-                if ((both[j] >> lane) & 1u) {
+                // a chain of pairs (own and partner cells left-linked) joins one
+                // pair of runs: their roots in the live forest are compared at
+                // the chain's head (bit 0 of a word always is one) and only
+                // chains that are still apart are tested
+                // (`filter`: not before the first cross-band unions, when bands
+                // are still apart anyway)
+                diff[j] = (both[j] >> lane) & 1u;
+                if (filter) {
+                    const uint32_t heads = both[j] & ~((both[j] << 1) & Ll[w[j]] & ltw[j]);
+                    bool hd = false;
+                    if ((heads >> lane) & 1u)
+                        hd = root(low_tag | run_of(SBl, NBl, w[j], lane)) !=
+                             root(((uint32_t)kt[j] << a.SHN) |
+                                  run_of(plane(SB, kt[j]), plane(NB, kt[j]), twr[j] + (tc[j] >> 5), tc[j] & 31));
+                    const uint32_t D = __ballot_sync(kFull, hd);
+                    const uint32_t hb = heads & lanemask_le(lane);
+                    diff[j] = diff[j] && hb && ((D >> (31 - __clz(hb))) & 1u);
+                }
+                if (diff[j]) {
                     vt[j] = __ldg(fr + (size_t)tr * W + tc[j]);
                     vo[j] = __ldg(fr + (size_t)r * W + cw * 32 + lane);
                     tco[j] = __ldg(a.tables + 6 * H - 5 + o * H + tr);
@@ -409,7 +429,7 @@ __device__ __forceinline__ void mc_axis_cross(const KArgs &a, const cg::cluster_
 #pragma unroll
             for (int j = 0; j < 2; ++j) {
                 if (!both[j]) continue;   // warp-uniform
-                const bool pass = ((both[j] >> lane) & 1u) && pair_pass(vt[j], vo[j], tco[j], a.dmax2);
+                const bool pass = diff[j] && pair_pass(vt[j], vo[j], tco[j], a.dmax2);
                 const uint32_t m = __ballot_sync(kFull, pass);
                 if (!m) continue;
                 // the pair to the left passed and joins the same runs
