@@ -388,10 +388,10 @@ __device__ __forceinline__ void mc_axis_cross(const KArgs &a, const cg::cluster_
                 w[j] = twr[j] = kt[j] = tc[j] = 0;
                 vo[j] = vt[j] = tco[j] = 0.f;
                 if (wi >= nq * WPR) continue;   // warp-uniform
-                const int q = wi / WPR, cw = wi - q * WPR;
+                const int q = divWPR(a, wi), cw = wi - q * WPR;
                 const int r = r0 + q, tr = r - dy;
                 if (tr < 0) continue;   // warp-uniform
-                kt[j] = tr / R;
+                kt[j] = r0 - tr <= R ? bl - 1 : tr / R;   // (the band above, unless dy > R)
                 // whose word is it?  shared pairs (partner row in band bl - 1) by halves
                 const bool shared = kt[j] == bl - 1;
                 if (lower ? (shared && cw < whalf) : !(shared && cw < whalf)) continue;
