@@ -864,6 +864,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
                     while (o1 < a.n_off && mc_axis_offset(a, o1)) ++o1;   // consecutive skip offsets share a round
                 mc_axis_heads(a, o0, o1, P, L, U, SB, NB, E, rows, tid, kFastThreads, SZ, lcap, cnt, chain);
                 __syncthreads();
+                RS_MARK(21);
                 const uint32_t nl = min(*cnt, lcap);   // block-uniform
                 for (uint32_t i = tid; i < nl; i += kFastThreads) {
                     const uint32_t e = SZ[2 * i], cells = SZ[2 * i + 1];
@@ -871,6 +872,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
                     chain(e, cells);
                 }
                 __syncthreads();
+                RS_MARK(23);
                 // every thread has read this round's counter: zero it for the round
                 // after the next (nobody touches it during the next round)
                 if (tid == 0) *cnt = 0;

@@ -31,6 +31,15 @@
 
 namespace rs {
 
+#ifdef RS_MC_STATS
+__device__ unsigned long long g_mcstats[8];
+#define RS_MCSTAT(i, v) atomicAdd(&g_mcstats[i], (unsigned long long)(v))
+#else
+#define RS_MCSTAT(i, v) \
+    do {                \
+    } while (0)
+#endif
+
 // The 32 bits of plane row `row` (W cells, WPR words) starting at cell t0
 // (wrapping at W; W % 32 == 0 for the funnel path).
 __device__ __forceinline__ uint32_t row_bits(const uint32_t *row, int t0, int W, int WPR, int lane, bool funnel) {
@@ -122,14 +131,6 @@ __device__ __forceinline__ void mc_pass(const KArgs &a, const cg::cluster_group 
 
 namespace rs {
 
-#ifdef RS_MC_STATS
-__device__ unsigned long long g_mcstats[8];
-#define RS_MCSTAT(i, v) atomicAdd(&g_mcstats[i], (unsigned long long)(v))
-#else
-#define RS_MCSTAT(i, v) \
-    do {                \
-    } while (0)
-#endif
 
 // Run end: the last cell of the run starting at bit b of word cw of a row
 // (left links continuing after it).
@@ -181,9 +182,18 @@ struct AxisWord {
     uint32_t cand, heads;
 };
 
-// candidate and chain-head bits of word w (row q of the band, word cw of the row) for axis offset o
+// candidate and chain-head bits of word w (row q of the band, word cw of the
+// row) for axis offset o.  Besides the broken straight chain, a pair is ruled
+// out when a detour of direct links one row (column) aside already joins its
+// cells — the usual case around a dropped cell on a surface:
+//   (0, k): both cells have an up edge and the row above is left-linked from
+//           c - k to c (or the same through the row below);
+//   (k, 0): both cells are left-linked to column c - 1 and that column has its
+//           k up edges (or the same through column c + 1).
+// (Bits that would need a neighbouring word are not ruled out.)
 __device__ __forceinline__ AxisWord mc_axis_word(const KArgs &a, const uint32_t *P, const uint32_t *L,
-                                                 const uint32_t *U, const uint32_t *SB, int o, int w, int q, int cw) {
+                                                 const uint32_t *U, const uint32_t *SB, int o, int w, int q, int cw,
+                                                 int rows) {
     const int WPR = a.WPR;
     const int dy = a.dy[o], k = a.dx[o] ? a.dx[o] : dy;
     const uint32_t pw = P[w];
@@ -197,11 +207,36 @@ __device__ __forceinline__ AxisWord mc_axis_word(const KArgs &a, const uint32_t 
         uint32_t diff = cw == 0 ? (1u << k) - 1u : 0u;
         for (int i = 0; i < k; ++i) diff |= (sb << i) | (i ? sbl >> (32 - i) : 0u);
         cand = pw & pt & diff;
+#ifndef RS_MC_NO_DETOUR
+        if (cand) {
+            // detour through the row above / below (bits k.. of the word only)
+            uint32_t det = 0;
+            if (q > 0) {
+                const uint32_t u = U[w], la = L[w - WPR];
+                uint32_t d = u & (u << k);
+                for (int i = 0; i < k; ++i) d &= la << i;
+                det |= d;
+            }
+            if (q + 1 < rows) {
+                const uint32_t u = U[w + WPR], lb = L[w + WPR];
+                uint32_t d = u & (u << k);
+                for (int i = 0; i < k; ++i) d &= lb << i;
+                det |= d;
+            }
+            cand &= ~(det & (~0u << k));
+        }
+#endif
     } else if (a.dx[o] == 0) {
-        ltw = L[w - dy * WPR];
+        const uint32_t lt = L[w - dy * WPR];
+        ltw = lt;
         uint32_t chain = ~0u;
         for (int i = 0; i < dy; ++i) chain &= U[w - i * WPR];
         cand = pw & P[w - dy * WPR] & ~chain;
+#ifndef RS_MC_NO_DETOUR
+        // detour through column c - 1 (bits 1..) or c + 1 (bits ..30)
+        const uint32_t both = L[w] & lt;
+        cand &= ~((both & (chain << 1)) | (((both & chain) >> 1) & 0x7fffffffu));
+#endif
     }
     return {cand, cand & ~((cand << 1) & L[w] & ltw)};
 }
@@ -240,9 +275,11 @@ __device__ __forceinline__ void mc_axis_heads(const KArgs &a, int o0, int o1, co
         for (int w = dy * WPR + tid; w < nw; w += nthreads) {   // rows q < dy: partner row in another band (or none)
             if (!P[w]) continue;
             const int q = divWPR(a, w), cw = w - q * WPR;
-            const AxisWord aw = axis ? mc_axis_word(a, P, L, U, SB, o, w, q, cw) : mc_any_word(a, P, L, o, w, q, cw);
+            const AxisWord aw = axis ? mc_axis_word(a, P, L, U, SB, o, w, q, cw, rows) : mc_any_word(a, P, L, o, w, q, cw);
             const uint32_t heads = aw.heads;
+            RS_MCSTAT(0, 1);
             if (!heads) continue;
+            RS_MCSTAT(1, __popc(heads));
             // heads whose two runs have different band-local roots (the words'
             // run counts stay in registers across the heads)
             const int tqw = (q - dy) * WPR;
@@ -253,6 +290,7 @@ __device__ __forceinline__ void mc_axis_heads(const KArgs &a, int o0, int o1, co
                 if (E[run_of(SB, NB, w, b)] != E[run_of(SB, NB, tqw + (tc >> 5), tc & 31)]) live |= 1u << b;
             }
             if (!live) continue;
+            RS_MCSTAT(2, __popc(live));
             uint32_t slot = atomicAdd(count, (uint32_t)__popc(live));
             for (uint32_t m = live; m; m &= m - 1, ++slot) {
                 const int b = __ffs(m) - 1;
@@ -339,7 +377,9 @@ __device__ __forceinline__ void mc_chain_finish(const KArgs &a, const uint32_t *
             for (int j = 0; j < 4; ++j) pass |= on[j] && pair_pass(vt[j], vo[j], c.tco, a.dmax2);
         }
     }
+    RS_MCSTAT(3, __popc(live));
     if (pass) {
+        RS_MCSTAT(4, 1);
         const int tc = mc_partner_col(cw * 32 + b, dx, W);
         unite(run_of(SB, NB, w, b), run_of(SB, NB, (q - dy) * WPR + (tc >> 5), tc & 31));
     }

@@ -23,4 +23,4 @@ for cid, pat in ((1, "S1"), (1, "mc6"), (1, "mc14"), (4, "S1")):
     pipe.segment_batch(frames)
     torch.cuda.synchronize()
     lib.rs_mc_stats(out, 1)
-    print(cid, pat, "items/run-offsets %d compared %d differ %d cells-tested %d unites %d" % tuple(out[:5]))
+    print(cid, pat, "words-with-cells %d heads %d live-chains %d chain-cells %d unions %d (per batch)" % tuple(out[:5]))

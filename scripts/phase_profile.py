@@ -63,14 +63,15 @@ ok = (buf[:, 19] > 0) & (buf[:, 20] > 0)
 for nm, i, j in sub:
     d2 = (buf[ok, j] - buf[ok, i]).astype(np.float64)
     print(f"  U.{nm:10s} mean {d2.mean():9.0f}  p90 {np.percentile(d2, 90):9.0f}")
-okb = (buf[:, 21] > 0) & (buf[:, 22] > 0) & (buf[:, 23] > 0)
+inband = (buf[:, 21] > 0) & (buf[:, 21] < buf[:, 6])   # Map Connections inside the band (marks before the size pass)
+okb = (buf[:, 21] > 0) & (buf[:, 22] > 0) & (buf[:, 23] > 0) & ~inband
 if okb.any():   # step M (Map Connections) inside "Z resolve"
     for nm, i, j in [("M.compress", 9, 21), ("M.runs", 21, 22), ("M.list unite", 22, 23), ("M.cs2b+Z", 23, 10)]:
         d3 = (buf[okb, j] - buf[okb, i]).astype(np.float64)
         print(f"  {nm:14s} mean {d3.mean():9.0f}  p90 {np.percentile(d3, 90):9.0f}  max {d3.max():9.0f}")
-oka = (buf[:, 21] > 0) & (buf[:, 22] > 0) & (buf[:, 23] == 0)
-if oka.any():   # skip offsets inside the band (mc_axis_list / mc_axis_cell), inside "U sizes"
-    for nm, i, j in [("axis.list", 5, 21), ("axis.unite+flat", 21, 22), ("sizes", 22, 6)]:
+oka = inband & (buf[:, 22] > 0) & (buf[:, 23] > 0)
+if oka.any():   # Map Connections inside the band (last round; inside "U sizes"): heads listed, chains tested + united, re-flatten
+    for nm, i, j in [("mc.heads (last round: 5 = first)", 5, 21), ("mc.chains", 21, 23), ("mc.reflatten", 23, 22), ("sizes", 22, 6)]:
         d3 = (buf[oka, j] - buf[oka, i]).astype(np.float64)
         print(f"  {nm:16s} mean {d3.mean():9.0f}  p90 {np.percentile(d3, 90):9.0f}  max {d3.max():9.0f}")
 C = pipe.ctas_per_frame
