@@ -177,6 +177,35 @@ def test_height_threshold_edges_vs_oracle(keep, rng, cuda):
         _assert_frame(res, b, wl, ws)
 
 
+@pytest.mark.parametrize("H,W,rows", [(32, 256, 4), (48, 2048, 16), (64, 1024, 0), (20, 96, 2), (36, 64, 8)])
+def test_in_band_map_connections_vs_oracle(H, W, rows, rng, cuda):
+    """Map Connections united inside the band (rs_mc.cuh: mc_axis_heads /
+    mc_chain_finish) and, for rows whose partner row lies in a band above,
+    during the cross-band step (mc_axis_cross): partner rows one and several
+    bands up (dy > rows_per_cta), horizontal offsets wider than a word,
+    negative dx across the azimuth seam, skip offsets with their detour
+    filter, many offsets (one round each), sparse speckle (long hook chains)
+    and a fully linked frame with holes (every chain united at once)."""
+    model = _random_model(H, W)
+    frames = rng.uniform(0.5, 12.0, size=(4, H, W)).astype(np.float32)
+    frames[rng.random(frames.shape) < 0.25] = 0
+    frames[1] = 7.0                               # everything linked ...
+    frames[1, :, ::3] = 0                         # ... but for every third column
+    frames[2] = 7.0
+    frames[2, 1::2, :] = 0                        # every second row missing: only (2k, 0) links rows
+    frames[3, rng.random((H, W)) < 0.6] = 0       # speckle
+    cand = ((0, 2), (2, 0), (0, 3), (3, 0), (9, 0), (5, 3), (0, 40), (7, -2), (1, -1), (2, 2), (17, 17),
+            (4, -33), (0, W // 2), (H - 1, 1))
+    offs = tuple(o for o in cand if o[0] < H and abs(o[1]) < W and (o[0] > 0 or o[1] > 0))
+    for cfg in (rs.PipelineConfig(ground_removal=False, min_cluster_points=1, mc_pattern=rs.MCPattern(offs)),
+                rs.PipelineConfig(ground_removal=False, min_cluster_points=2, mc_pattern=rs.skip_pattern(3)),
+                rs.PipelineConfig(min_cluster_points=5, mc_pattern=rs.MCPattern(((2, 0), (4, 0), (1, 1))))):
+        pipe, res = _run(model, cfg, frames, rows_per_cta=rows)
+        for b in range(frames.shape[0]):
+            wl, ws = oracle.segment_frame(frames[b], pipe.packed)
+            _assert_frame(res, b, wl, ws)
+
+
 @pytest.mark.parametrize("H,W,rows", [(64, 2048, 0), (33, 300, 8), (40, 96, 16), (24, 4096, 0)])
 def test_step_a_map_connections_vs_oracle(H, W, rows, rng, cuda):
     """Offsets with dy <= 2 and 0 <= dx <= 31 (at most four) are tested in
