@@ -240,6 +240,39 @@ struct BitsStrip {
 #endif
             np += rowf;
         }
+        const bool halo = HALO;   // only the first row walked in a band > 0 (peeled in run())
+        const int cw = ch * 4;
+        const uint32_t off = halo ? 0u : (uint32_t)((r - r0) * wpb);
+#ifndef RS_NO_EMPTY_SKIP
+        {
+            // input-contract screen on the row being decided (every row of the
+            // walk is the current row exactly once; its values are in registers
+            // by now): the unsigned maximum of the raw bits (VIMNMX3) ...
+            const uint32_t t = max(__vimax3_u32(__float_as_uint(v[0]), __float_as_uint(v[1]), __float_as_uint(v[2])),
+                                   __float_as_uint(v[3]));
+            mx = max(mx, t);
+            // ... which also tells when the chunk's 128 cells of this row are
+            // all +0.0 (no return: sky, beyond the range cut): no cell is
+            // present, so the row's three plane words are zero whatever the
+            // pair tests say (step B masks them with presence), and the rules
+            // are skipped
+            if (!__any_sync(kFull, t != 0u)) {
+                if (FULL) {
+                    if (lane == 0) {
+                        sts128((halo ? sPh : sP) + off, 0u, 0u, 0u, 0u);
+                        sts128((halo ? sLh : sL) + off, 0u, 0u, 0u, 0u);
+                        if (!halo) sts128(sU + off, 0u, 0u, 0u, 0u);
+                    }
+                } else if (lane < 4 && cw + lane < a.WPR) {
+                    const uint32_t lo = off + 4u * (uint32_t)lane;
+                    sts32((halo ? sPh : sP) + lo, 0u);
+                    sts32((halo ? sLh : sL) + lo, 0u);
+                    if (!halo) sts32(sU + lo, 0u);
+                }
+                return;
+            }
+        }
+#endif
         const float4 c = *reinterpret_cast<const float4 *>(rowc + (r - rstart) * 8);
         const float4 c2 = *reinterpret_cast<const float4 *>(rowc + (r - rstart) * 8 + 4);
         const int srcl = (lane + 31) & 31;
@@ -258,16 +291,13 @@ struct BitsStrip {
             lw[j] = __ballot_sync(kFull, pair_pass(vl, v[j], tch, thr));
             uw[j] = ROW0 ? 0u : __ballot_sync(kFull, pair_pass(va[j], v[j], c2.y, thr));
         }
-#ifndef RS_NO_SCREEN
+#ifdef RS_NO_EMPTY_SKIP
         // input-contract screen on the row just decided (every row of the walk
         // is the current row exactly once; its values are in registers by
         // now): two 3-input unsigned max (VIMNMX3) for the lane's four cells
         mx = __vimax3_u32(mx, __float_as_uint(v[0]), __float_as_uint(v[1]));
         mx = __vimax3_u32(mx, __float_as_uint(v[2]), __float_as_uint(v[3]));
 #endif
-        const bool halo = HALO;   // only the first row walked in a band > 0 (peeled in run())
-        const int cw = ch * 4;
-        const uint32_t off = halo ? 0u : (uint32_t)((r - r0) * wpb);
         if (FULL) {
             if (lane == 0) {
                 sts128((halo ? sPh : sP) + off, pw[0], pw[1], pw[2], pw[3]);
