@@ -9,17 +9,19 @@
 //      each warp walks a 128-column chunk down the band, keeping the row above
 //      in registers and prefetching two rows ahead (the reference's float32
 //      rules, one rounding per op: ground.py:112-140, connectivity.py:47-92);
-//      Map Connection offsets with dy <= 2, 0 <= dx <= 31 are tested here too
-//      (rs_fast_kernel<true>).
+//      a chunk row without any return skips the rules (in the kernel without
+//      Map Connections: in the other the extra test costs more than it saves).
 //   B  presence masking of the edge words, chunk-boundary left bits, the
-//      seam, the remaining Map Connection bits.
+//      seam.
 //   R  runs: start bits, and a block scan of their counts that numbers the
 //      runs of the band 0..n-1 in cell order (run id order == cell order).
 //   U  band-local union-find over run ids in shared memory: non-redundant
 //      edges listed, every run hooked under its smallest listed neighbour,
-//      then all edges united (path halving); local flatten; run lengths
-//      added to local roots.
-//   X  cross-band unions over DSMEM (boundary edges listed, then united).
+//      then all edges united (path halving); local flatten; Map Connections
+//      inside the band (rs_fast_kernel<true>, rs_mc.cuh); run lengths added
+//      to local roots.
+//   X  cross-band unions over DSMEM (boundary edges and cross-band Map
+//      Connection pairs listed, then united).
 //   Z  every band-local root resolves its global root and adds its size there.
 //   K  kept roots (size >= min_points): kept bits and word prefixes per band,
 //      band bases -> label = 1 + rank of the component's first cell among kept
@@ -194,7 +196,7 @@ struct RunUF {
 // 16-byte stores of the four words by lane 0).  GROUND: ground removal on.
 // Plane stores use 32-bit shared-memory byte addresses (sP/sL/sU: the chunk's
 // words in the band's first row; sPh/sLh: the halo row).
-template <bool FULL, bool GROUND, bool RING = false>
+template <bool FULL, bool GROUND, bool RING = false, bool SKIP = true>
 struct BitsStrip {
     const KArgs &a;
     const float *col;
@@ -244,7 +246,7 @@ struct BitsStrip {
         const int cw = ch * 4;
         const uint32_t off = halo ? 0u : (uint32_t)((r - r0) * wpb);
 #ifndef RS_NO_EMPTY_SKIP
-        {
+        if (SKIP) {
             // input-contract screen on the row being decided (every row of the
             // walk is the current row exactly once; its values are in registers
             // by now): the unsigned maximum of the raw bits (VIMNMX3) ...
@@ -292,12 +294,17 @@ struct BitsStrip {
             uw[j] = ROW0 ? 0u : __ballot_sync(kFull, pair_pass(va[j], v[j], c2.y, thr));
         }
 #ifdef RS_NO_EMPTY_SKIP
-        // input-contract screen on the row just decided (every row of the walk
-        // is the current row exactly once; its values are in registers by
-        // now): two 3-input unsigned max (VIMNMX3) for the lane's four cells
-        mx = __vimax3_u32(mx, __float_as_uint(v[0]), __float_as_uint(v[1]));
-        mx = __vimax3_u32(mx, __float_as_uint(v[2]), __float_as_uint(v[3]));
+        constexpr bool kScreenHere = true;
+#else
+        constexpr bool kScreenHere = !SKIP;
 #endif
+        if (kScreenHere) {
+            // input-contract screen on the row just decided (every row of the
+            // walk is the current row exactly once; its values are in registers
+            // by now): two 3-input unsigned max (VIMNMX3) for the lane's four cells
+            mx = __vimax3_u32(mx, __float_as_uint(v[0]), __float_as_uint(v[1]));
+            mx = __vimax3_u32(mx, __float_as_uint(v[2]), __float_as_uint(v[3]));
+        }
         if (FULL) {
             if (lane == 0) {
                 sts128((halo ? sPh : sP) + off, pw[0], pw[1], pw[2], pw[3]);
@@ -583,8 +590,8 @@ __global__ void __launch_bounds__(kFastThreads, kFastOcc) rs_fast_kernel(const _
             const bool full = ch * 128 + 128 <= W && (WPR & 3) == 0;
 #define RS_STRIP(F, G)                                                                                          \
     do {                                                                                                    \
-        const BitsStrip<F, G> st{a, fr + cb, rowc, sP, sL, sU, sPh, sLh, ch, lane, r0, rstart, rhi, cb, thr, \
-                                      tch, rlo, W, 4 * WPR};                                            \
+        const BitsStrip<F, G, false, !MC> st{a, fr + cb, rowc, sP, sL, sU, sPh, sLh, ch, lane, r0, rstart, rhi, cb, \
+                                             thr, tch, rlo, W, 4 * WPR};                                  \
         st.run();                                                                                           \
         umx = max(umx, st.mx);                                                                              \
     } while (0)

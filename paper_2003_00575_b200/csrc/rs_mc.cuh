@@ -8,23 +8,27 @@
 // clusters.  The result is the connected components of the graph (present
 // cells; direct edges plus every passing Map Connection pair).
 //
-// The fused kernel does the same once its direct-edge forest is final
-// (barrier #2) and every run points straight at its root: a pair is tested
-// only if its two cells have different roots — the reference's "labels
-// differ".  Pairs come in chains: along a row, consecutive candidate pairs
-// whose own cells and partner cells are left-linked join the same two runs,
-// so the roots are compared once per chain (at its head) and the verdict is
-// shared along the chain.  Most chains lie inside one component, so few
-// ranges are loaded at all; passing pairs go into the same cluster-wide
-// union-find as the other edges.  Presence and left-link bits of the partner
-// row are built a word at a time (a funnel shift of two plane words, local or
-// over DSMEM).  No per-offset bit plane is kept in shared memory, so the band
-// layout (and the two-CTAs-per-SM occupancy) is the same with any number of
-// offsets.
+// The fused kernel builds that graph in one forest.  Any passing pair may be
+// united at any time (the unions commute), and a pair whose cells are already
+// in one component need not be tested — the reference's "labels differ".
+// Pairs come in chains: along a row, consecutive candidate pairs whose own
+// cells and partner cells are left-linked join the same two runs, so the
+// roots are compared once per chain (at its head) and the chain is united
+// once, at its first passing cell.  Presence and left-link bits of the
+// partner row are built a word at a time (a funnel shift of two plane words,
+// local or over DSMEM).  No per-offset bit plane is kept in shared memory, so
+// the band layout (and the two-CTAs-per-SM occupancy) is the same with any
+// number of offsets.
 //
-// With `out` set (rs_fast_planes), or without ROOTS (the overflow path),
-// every present pair is tested; `out` then receives the decision words as
-// plane 3 + o of the frame.
+//   * inside the band, before barrier #1 (production path, widths that are
+//     whole words): mc_axis_heads lists the chains whose runs have different
+//     band-local roots, mc_chain_issue / mc_chain_finish test and unite them,
+//     spread evenly over the CTA; the caller re-flattens the forest;
+//   * rows whose partner row lies in a band above: mc_axis_cross, a lane per
+//     cell during the cross-band step, passing pairs join that step's list;
+//   * after barrier #2 (mc_runs: other widths) / mc_pass (the parity export
+//     rs_fast_planes and the overflow path, where every present pair is tested
+//     and `out` receives the decision words as plane 3 + o of the frame).
 #pragma once
 
 #include "rs_common.cuh"
