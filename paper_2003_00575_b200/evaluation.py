@@ -139,45 +139,71 @@ def contingency_device_ms(gt: torch.Tensor, pred: torch.Tensor, offsets: torch.T
     return a.elapsed_time(b) / reps
 
 
-def _match_table(g_ids, c_ids, cnt, cfg: EvalConfig):
-    """The reference's matching rules (evaluation.py:79-129) over one frame's
-    contingency table (gt ids, cluster ids, counts; 0 = none)."""
-    gt_size, pred_size = {}, {}
-    for g, c, n in zip(g_ids.tolist(), c_ids.tolist(), cnt.tolist()):
-        if g > 0:
-            gt_size[g] = gt_size.get(g, 0) + n
-        if c > 0:
-            pred_size[c] = pred_size.get(c, 0) + n
-    scored = sorted(g for g, n in gt_size.items() if n >= cfg.min_gt_points)
-    if not scored:
-        return []
-    overlaps = {}
-    for g, c, n in zip(g_ids.tolist(), c_ids.tolist(), cnt.tolist()):
-        if g > 0 and c > 0:
-            overlaps.setdefault(g, []).append((c, n))   # clusters ascending within g
-    best = {}
-    for g in scored:
-        ov = overlaps.get(g, [])
-        if not ov:
-            best[g] = (None, 0.0)
-            continue
-        iou = {c: n / (gt_size[g] + pred_size[c] - n) for c, n in ov}
-        if sum(1 for v in iou.values() if v > 0.5) > 1:
-            raise RuntimeError(f"instance {g} overlaps two clusters with IoU > 0.5; "
+def _match_tables(f_ids, g_ids, c_ids, cnt, n_frames: int, cfg: EvalConfig):
+    """The reference's matching rules (evaluation.py:79-129) over the contingency
+    tables of ``n_frames`` frames at once (frame, gt id, cluster id, count; id 0 =
+    none), vectorised: per scored instance the cluster with the most common
+    points (then the higher IoU, then the lower cluster id), IoU as the same
+    float64 quotient of integers; a cluster claimed by several instances goes
+    to the highest IoU (then the lower instance id).  One list per frame."""
+    f = np.asarray(f_ids, dtype=np.int64)
+    g = np.asarray(g_ids, dtype=np.int64)
+    c = np.asarray(c_ids, dtype=np.int64)
+    n = np.asarray(cnt, dtype=np.int64)
+    out = [[] for _ in range(n_frames)]
+    K = 1 << _LABEL_BITS
+    mg = g > 0
+    if not mg.any():
+        return out
+    ug, inv_g = np.unique(f[mg] * K + g[mg], return_inverse=True)   # instances, by (frame, id)
+    gsz = np.zeros(ug.size, dtype=np.int64)
+    np.add.at(gsz, inv_g, n[mg])
+    scored = gsz >= cfg.min_gt_points
+    if not scored.any():
+        return out
+    mc = c > 0
+    uc, inv_c = np.unique(f[mc] * K + c[mc], return_inverse=True)   # clusters, by (frame, id)
+    csz = np.zeros(uc.size, dtype=np.int64)
+    np.add.at(csz, inv_c, n[mc])
+    best_c = np.zeros(ug.size, dtype=np.int64)        # 0 = no overlapping cluster
+    best_v = np.zeros(ug.size, dtype=np.float64)
+    mo = mg & mc
+    ig = np.searchsorted(ug, f[mo] * K + g[mo])
+    keep = scored[ig]
+    ig, co, no = ig[keep], c[mo][keep], n[mo][keep]
+    if ig.size:
+        ic = np.searchsorted(uc, (ug[ig] // K) * K + co)
+        iou = no / (gsz[ig] + csz[ic] - no)
+        twice = np.bincount(ig[iou > 0.5], minlength=ug.size) > 1
+        if twice.any():
+            raise RuntimeError(f"instance {int(ug[np.argmax(twice)] % K)} overlaps two clusters with IoU > 0.5; "
                                "predicted clusters are not disjoint")
-        c_best = max(ov, key=lambda cn: (cn[1], iou[cn[0]], -cn[0]))[0]
-        best[g] = (c_best, iou[c_best])
-    claims = {}
-    for g, (c, v) in best.items():
-        if c is not None:
-            claims.setdefault(c, []).append((g, v))
-    out = []
-    for g in scored:
-        c, v = best[g]
-        if c is not None and max(claims[c], key=lambda gv: (gv[1], -gv[0]))[0] != g:
-            c, v = None, 0.0
-        out.append(InstanceMatch(gt_id=int(g), matched_cluster=c, iou=v))
+        # the maximum of (count, IoU, -cluster id) per instance: last of its group in that order
+        order = np.lexsort((-co, iou, no, ig))
+        last = np.r_[ig[order][1:] != ig[order][:-1], True]
+        pick = order[last]
+        best_c[ig[pick]] = co[pick]
+        best_v[ig[pick]] = iou[pick]
+        # a cluster claimed more than once: the maximum of (IoU, -instance id) keeps it
+        cl = np.flatnonzero(best_c > 0)
+        ckey = (ug[cl] // K) * K + best_c[cl]
+        order = np.lexsort((-(ug[cl] % K), best_v[cl], ckey))
+        last = np.r_[ckey[order][1:] != ckey[order][:-1], True]
+        lost = np.ones(cl.size, dtype=bool)
+        lost[order[last]] = False
+        best_c[cl[lost]] = 0
+        best_v[cl[lost]] = 0.0
+    for i in np.flatnonzero(scored).tolist():
+        key = int(ug[i])
+        cb = int(best_c[i])
+        out[key // K].append(InstanceMatch(gt_id=key % K, matched_cluster=cb if cb else None,
+                                           iou=float(best_v[i]) if cb else 0.0))
     return out
+
+
+def _match_table(g_ids, c_ids, cnt, cfg: EvalConfig):
+    """One frame's contingency table (gt ids, cluster ids, counts; 0 = none)."""
+    return _match_tables(np.zeros(len(g_ids), dtype=np.int64), g_ids, c_ids, cnt, 1, cfg)[0]
 
 
 def match_instances_batch(gt: torch.Tensor, pred: torch.Tensor, offsets: torch.Tensor,
@@ -185,10 +211,7 @@ def match_instances_batch(gt: torch.Tensor, pred: torch.Tensor, offsets: torch.T
     """``match_instances`` for B frames of per-point labels on the device."""
     cfg = cfg or EvalConfig()
     f, g, c, n = contingency_batch(gt, pred, offsets)
-    B = offsets.numel() - 1
-    bounds = np.searchsorted(f, np.arange(B + 1))
-    return [_match_table(g[bounds[b]:bounds[b + 1]], c[bounds[b]:bounds[b + 1]],
-                         n[bounds[b]:bounds[b + 1]], cfg) for b in range(B)]
+    return _match_tables(f, g, c, n, offsets.numel() - 1, cfg)
 
 
 def match_instances(gt_instance_ids, pred_labels, cfg: EvalConfig | None = None):
