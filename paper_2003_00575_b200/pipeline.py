@@ -365,15 +365,27 @@ class Pipeline:
         if self._frame_bufs is None:
             H, W = self.shape
             pin = dict(pin_memory=True)
+            # the three outputs share one device block and one pinned block (labels,
+            # then sizes, then the count; 16-byte aligned parts), so that one D2H
+            # copy brings all of them back
+            nl = H * W * 4
+            o_sz = (nl + 15) & ~15
+            o_ncl = o_sz + ((self.sizes_stride * 8 + 15) & ~15)
+            total = o_ncl + 16
+
+            def views(blk):
+                return (blk[:nl].view(torch.int32).view(1, H, W),
+                        blk[o_sz:o_sz + self.sizes_stride * 8].view(torch.int64).view(1, self.sizes_stride),
+                        blk[o_ncl:o_ncl + 4].view(torch.int32))
+            h_out = torch.empty((total,), dtype=torch.uint8, **pin)
+            d_out = torch.empty((total,), dtype=torch.uint8, device=self.device)
+            h_lab, h_sz, h_ncl = views(h_out)
+            d_lab, d_sz, d_ncl = views(d_out)
             self._frame_bufs = {
                 "h_in": torch.empty((1, H, W), dtype=torch.float32, **pin),
-                "h_lab": torch.empty((1, H, W), dtype=torch.int32, **pin),
-                "h_ncl": torch.empty((1,), dtype=torch.int32, **pin),
-                "h_sz": torch.empty((1, self.sizes_stride), dtype=torch.int64, **pin),
+                "h_out": h_out, "h_lab": h_lab, "h_ncl": h_ncl, "h_sz": h_sz,
                 "d_in": torch.empty((1, H, W), dtype=torch.float32, device=self.device),
-                "d_lab": torch.empty((1, H, W), dtype=torch.int32, device=self.device),
-                "d_ncl": torch.empty((1,), dtype=torch.int32, device=self.device),
-                "d_sz": torch.empty((1, self.sizes_stride), dtype=torch.int64, device=self.device),
+                "d_out": d_out, "d_lab": d_lab, "d_ncl": d_ncl, "d_sz": d_sz,
                 "ev": [torch.cuda.Event(enable_timing=True) for _ in range(3)],
             }
         return self._frame_bufs
@@ -414,9 +426,7 @@ class Pipeline:
                 ctypes.c_void_p(s.cuda_stream))
             _native.check(st, "rs_segment_batch")
             ev[1].record(s)
-            b["h_lab"].copy_(b["d_lab"], non_blocking=True)
-            b["h_ncl"].copy_(b["d_ncl"], non_blocking=True)
-            b["h_sz"].copy_(b["d_sz"], non_blocking=True)
+            b["h_out"].copy_(b["d_out"], non_blocking=True)   # labels, sizes and count in one copy
             ev[2].record(s)
             ev[2].synchronize()
         if self.stage_timing:
