@@ -195,11 +195,12 @@ struct AxisWord {
 //   (k, 0): both cells are left-linked to column c - 1 and that column has its
 //           k up edges (or the same through column c + 1).
 // (Bits that would need a neighbouring word are not ruled out.)
-__device__ __forceinline__ AxisWord mc_axis_word(const KArgs &a, const uint32_t *P, const uint32_t *L,
-                                                 const uint32_t *U, const uint32_t *SB, int o, int w, int q, int cw,
-                                                 int rows) {
+template <int KC>   // KC > 0: the offset's k as a compile-time constant (loops unrolled), 0: any k
+__device__ __forceinline__ AxisWord mc_axis_word_k(const KArgs &a, const uint32_t *P, const uint32_t *L,
+                                                   const uint32_t *U, const uint32_t *SB, int o, int w, int q, int cw,
+                                                   int rows) {
     const int WPR = a.WPR;
-    const int dy = a.dy[o], k = a.dx[o] ? a.dx[o] : dy;
+    const int dy = KC ? (a.dy[o] ? KC : 0) : a.dy[o], k = KC ? KC : (a.dx[o] ? a.dx[o] : dy);
     const uint32_t pw = P[w];
     uint32_t cand = 0, ltw = 0;
     if (dy == 0) {
@@ -243,6 +244,15 @@ __device__ __forceinline__ AxisWord mc_axis_word(const KArgs &a, const uint32_t 
 #endif
     }
     return {cand, cand & ~((cand << 1) & L[w] & ltw)};
+}
+
+__device__ __forceinline__ AxisWord mc_axis_word(const KArgs &a, const uint32_t *P, const uint32_t *L,
+                                                 const uint32_t *U, const uint32_t *SB, int o, int w, int q, int cw,
+                                                 int rows) {
+    // BASELINE's S = 1 is k = 2 on both axes: its loops unrolled
+    const int k = a.dx[o] ? a.dx[o] : a.dy[o];
+    return k == 2 ? mc_axis_word_k<2>(a, P, L, U, SB, o, w, q, cw, rows)
+                  : mc_axis_word_k<0>(a, P, L, U, SB, o, w, q, cw, rows);
 }
 
 // the same for any other offset (no straight chain of links to rule pairs
